@@ -1,0 +1,146 @@
+/*
+ * lowbit_cuda.h — C ABI of the B200 (sm_100a) low-bit GeMM library
+ * (paper_2205_09120_b200/liblowbit_cuda.so).
+ *
+ * This is the drop-in boundary for the reference library `lowbit`
+ * (/root/reference/proj, namespace lowbit, headers include/lowbit/*.hpp).
+ * Every entry point names the reference interface it replaces.  Plain C:
+ * pointers, sizes and status codes only; no C++ or torch types.  The C++
+ * drop-in (paper_2205_09120_b200/cpp, namespace lowbit) and the Python
+ * bindings sit on top of these symbols; INTEGRATION.md shows how a
+ * maintainer binds them.
+ *
+ * Conventions
+ *  - Device-pointer entry points are stream-ordered on `stream` (a
+ *    cudaStream_t; NULL = legacy default stream), do not synchronise and do
+ *    not allocate.  They are safe to call from several host threads on
+ *    distinct streams.
+ *  - Bit planes use the reference encoding (core.hpp:3-10): LSB-first bytes,
+ *    binary +1 -> 0 / -1 -> 1, ternary plus/minus planes.  On the device a
+ *    plane row starts every `pitch` bytes; pitch must be a multiple of 16
+ *    and >= ceil(cols/8); bytes past ceil(cols/8) must be zero
+ *    (lowbit_encode writes them so).  lowbit_plane_pitch() gives the
+ *    canonical pitch.
+ *  - Errors: the reference throws lowbit::Error subclasses (errors.hpp:8-45)
+ *    in the order check_cfg -> mode -> check_dims (gemm.cpp:81-84, 94-100).
+ *    Here each call returns the matching lowbit_status, checked in the same
+ *    order, and records a message plus detail values (e.g. k and k_max for
+ *    LOWBIT_DEPTH_OVERFLOW) readable with lowbit_last_error*().
+ */
+#ifndef LOWBIT_CUDA_H
+#define LOWBIT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOWBIT_ABI_VERSION 1
+#define LOWBIT_K_MAX16 32767 /* kernels.hpp:24 kMaxDepth16 */
+
+typedef enum lowbit_status {
+    LOWBIT_OK = 0,
+    LOWBIT_ERROR = 1,              /* lowbit::Error (e.g. bad k_blk, gemm.cpp:9-12) */
+    LOWBIT_ZERO_IN_BINARY = 2,     /* lowbit::ZeroInBinaryInput (core.cpp:23) */
+    LOWBIT_INVALID_CODE = 3,       /* lowbit::InvalidCode */
+    LOWBIT_OUT_OF_BOUNDS = 4,      /* lowbit::OutOfBounds */
+    LOWBIT_DEPTH_OVERFLOW = 5,     /* lowbit::DepthOverflow(k, k_max) */
+    LOWBIT_MODE_MISMATCH = 6,      /* lowbit::ModeMismatch */
+    LOWBIT_CHANNEL_OVERFLOW = 7,   /* lowbit::ChannelOverflow(c_in, c_in_max) */
+    LOWBIT_EMPTY_OUTPUT = 8,       /* lowbit::EmptyOutput */
+    LOWBIT_CUDA_ERROR = 9,         /* CUDA runtime/driver failure (no reference analogue) */
+    LOWBIT_INVALID_ARGUMENT = 10,  /* device-layout precondition violated (pitch, alignment, NULL) */
+    LOWBIT_NO_DEVICE = 11          /* no sm_100 device visible: the library has no CPU fallback */
+} lowbit_status;
+
+/* gemm.hpp:24 GemmMode, same order. */
+typedef enum lowbit_gemm_mode { LOWBIT_BNN = 0, LOWBIT_TNN = 1, LOWBIT_TBN = 2 } lowbit_gemm_mode;
+
+/* Kernel choice for lowbit_gemm.  AUTO consults the static per-shape table
+ * (lowbit_select_kernel); the others force one kernel (tests, profiling). */
+typedef enum lowbit_kernel {
+    LOWBIT_KERNEL_AUTO = 0,
+    LOWBIT_KERNEL_BITSERIAL = 1, /* K2: LOP3 + POPC, int32 registers */
+    LOWBIT_KERNEL_TENSOR = 2     /* K3: tcgen05.mma kind::i8, int32 TMEM accumulators */
+} lowbit_kernel;
+
+typedef void* lowbit_stream; /* cudaStream_t */
+
+/* ---- library / errors --------------------------------------------------- */
+int lowbit_abi_version(void);
+const char* lowbit_status_string(int status);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* lowbit_last_error(void);
+/* Detail values of the last failure: DEPTH_OVERFLOW -> (k, k_max),
+ * CHANNEL_OVERFLOW -> (c_in, c_in_max); otherwise (0, 0). */
+void lowbit_last_error_values(long long* v0, long long* v1);
+/* LOWBIT_OK when an sm_100 device is present, else LOWBIT_NO_DEVICE. */
+lowbit_status lowbit_device_check(void);
+
+/* ---- layouts ------------------------------------------------------------ */
+/* Canonical device pitch for a plane with `cols` logical columns:
+ * round_up(ceil(cols/8), 16) bytes. */
+long long lowbit_plane_pitch(int cols);
+
+/* ---- K1: encode (core.hpp:63 encode_binary, core.hpp:66 encode_ternary) --
+ * values: rows x cols int8, row stride ld (elements), device.
+ * ternary=0: plane0 <- binary plane (-1 -> 1); a 0 element sets *zero_flag
+ *            to 1 (the caller raises ZeroInBinaryInput, core.cpp:23).
+ * ternary=1: plane0 <- plus plane, plane1 <- minus plane.
+ * Writes whole rows of `pitch` bytes (padding bytes zero).  zero_flag may be
+ * NULL for ternary; it is only ever set, never cleared. */
+lowbit_status lowbit_encode(int ternary, const int8_t* values, int rows, int cols, long long ld, uint8_t* plane0,
+                            uint8_t* plane1, long long pitch, int* zero_flag, lowbit_stream stream);
+
+/* ---- K1b: pack_b (gemm.hpp:75-76; pack.cpp:64-127) ------------------------
+ * b0/b1: K x N plane(s) packed along N (the reference B layout), row pitch
+ * `pitch` bytes (any pitch >= ceil(n/8) here).  panels: the reference
+ * PackedB byte stream — ceil(n/8) panels of group*ceil(k/8) bytes each,
+ * group 8 (bnn_b) or 16 (tnn_b), concatenated in panel order. */
+size_t lowbit_packed_b_bytes(int ternary, int n, int k);
+lowbit_status lowbit_pack_b(int ternary, const uint8_t* b0, const uint8_t* b1, int k, int n, long long pitch,
+                            uint8_t* panels, lowbit_stream stream);
+
+/* ---- weight preparation (no reference analogue: the GPU operand of PackedB)
+ * Turns PackedB panels into the device operand read by both GeMM kernels:
+ * an int8 K-major copy (tensor-core path) and K-major (nonzero, sign) bit
+ * words (bit-serial path).  Done once per weight matrix. */
+size_t lowbit_weights_bytes(int ternary, int n, int k);
+lowbit_status lowbit_prepare_weights(int ternary, const uint8_t* panels, int n, int k, void* weights,
+                                     lowbit_stream stream);
+
+/* ---- K2/K3: gemm_lowbit (gemm.hpp:78-81; gemm.cpp:79-112) ----------------
+ * mode: lowbit_gemm_mode.  a0 (+a1 for ternary A; a1 == NULL means a binary
+ * A) are a_rows x a_cols planes with pitch a_pitch.  weights: the output of
+ * lowbit_prepare_weights for a b_n x b_k PackedB of kind b_ternary.  dims
+ * (m, n, k) and k_blk are validated exactly like the reference (k_blk has
+ * no effect on results, gemm.cpp:32; the GPU ignores it after validation).
+ * c: m x n int16, row stride ldc elements.  kernel: lowbit_kernel. */
+lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int a_rows, int a_cols,
+                          const void* weights, int b_ternary, int b_n, int b_k, int m, int n, int k, int k_blk,
+                          int16_t* c, long long ldc, int kernel, lowbit_stream stream);
+
+/* The static per-shape kernel table behind LOWBIT_KERNEL_AUTO. */
+int lowbit_select_kernel(int mode, int m, int n, int k);
+
+/* ---- host-buffer drop-in: one whole reference gemm_lowbit call -----------
+ * Host A planes with the reference stride ceil(a_cols/8); host PackedB
+ * panels; host C (m x n, row-major).  Uploads, prepares B, runs, downloads
+ * and synchronises `stream`.  Device scratch is cached per host thread. */
+lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t* a1, int a_rows, int a_cols,
+                                      const uint8_t* panels, int b_ternary, int b_n, int b_k, int m, int n, int k,
+                                      int k_blk, int16_t* c, int kernel, lowbit_stream stream);
+
+/* ---- synthetic data (bench/tests): counter-based generator --------------
+ * out[r][c] = f_dist(splitmix64(seed ^ matrix_id<<56 ^ ((row0+r)*cols + c)))
+ * dist 0: uniform {-1,0,+1}; 1: uniform {-1,+1}; 2: P(0)=1/2, P(+-1)=1/4. */
+lowbit_status lowbit_generate(int dist, unsigned long long seed, int matrix_id, long long row0, long long rows,
+                              long long cols, int8_t* out, lowbit_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOWBIT_CUDA_H */

@@ -1,0 +1,179 @@
+"""Python host mirror of the reference `lowbit` API over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/lowbit/{core,pack,gemm}.hpp); device buffers are
+torch CUDA tensors (torch is plumbing here: memory, streams).  Every compute
+call goes through liblowbit_cuda.so — there is no CPU path.
+
+    encode_binary / encode_ternary   core.hpp:63,66   -> Planes (device bit planes)
+    pack_b                           gemm.hpp:75-76   -> PackedB (reference panel bytes, device)
+    prepare_weights                  (GPU operand of PackedB; once per weight matrix)
+    gemm_lowbit                      gemm.hpp:78-81   -> int16 [m, n] (device)
+    gemm_lowbit_host                 host-buffer drop-in of the whole call
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Union
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import BNN, TNN, TBN, KERNEL_AUTO, KERNEL_BITSERIAL, KERNEL_TENSOR  # noqa: F401
+
+GemmMode = {"bnn": BNN, "tnn": TNN, "tbn": TBN}
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def plane_pitch(cols: int) -> int:
+    return int(L.lib.lowbit_plane_pitch(cols))
+
+
+@dataclass
+class Planes:
+    """Device bit planes (BinaryPackedMatrix / TernaryPackedMatrix, core.hpp:36-61).
+
+    plane0 is the binary plane or the plus plane; plane1 the minus plane
+    (None for binary).  Rows are `pitch` bytes (multiple of 16)."""
+    rows: int
+    cols: int
+    plane0: torch.Tensor
+    plane1: Optional[torch.Tensor]
+
+    @property
+    def ternary(self) -> bool:
+        return self.plane1 is not None
+
+    @property
+    def pitch(self) -> int:
+        return int(self.plane0.stride(0))
+
+    @property
+    def stride_bits(self) -> int:  # core.hpp:38
+        return (self.cols + 7) // 8 * 8
+
+
+@dataclass
+class PackedB:
+    """Reference PackedB (gemm.hpp:67-73): ceil(n/8) panels concatenated, on device."""
+    ternary: bool
+    n: int
+    k: int
+    panels: torch.Tensor
+
+
+@dataclass
+class Weights:
+    """PackedB prepared for the GPU kernels (csrc/layout.cuh)."""
+    ternary: bool
+    n: int
+    k: int
+    buf: torch.Tensor
+
+
+def empty_planes(rows: int, cols: int, ternary: bool, device="cuda") -> Planes:
+    pitch = plane_pitch(cols)
+    p0 = torch.zeros((rows, pitch), dtype=torch.uint8, device=device)
+    p1 = torch.zeros((rows, pitch), dtype=torch.uint8, device=device) if ternary else None
+    return Planes(rows, cols, p0, p1)
+
+
+def _encode(values: torch.Tensor, ternary: bool, check_zero: bool = True) -> Planes:
+    if values.dtype != torch.int8 or not values.is_cuda or values.dim() != 2:
+        raise L.InvalidArgument("encode: expected a 2-D int8 CUDA tensor")
+    if values.stride(1) != 1:
+        values = values.contiguous()
+    rows, cols = values.shape
+    out = empty_planes(rows, cols, ternary, values.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=values.device)
+    L.check(L.lib.lowbit_encode(int(ternary), _ptr(values), rows, cols, values.stride(0), _ptr(out.plane0),
+                                _ptr(out.plane1), out.pitch, _ptr(flag), _stream()), "encode")
+    if not ternary and check_zero and rows and cols and int(flag.item()):
+        raise L.ZeroInBinaryInput("binary matrix contains a zero element")
+    return out
+
+
+def encode_binary(values: torch.Tensor, check_zero: bool = True) -> Planes:
+    """core.cpp:13-28 (+1 -> 0, -1 -> 1; a 0 raises ZeroInBinaryInput)."""
+    return _encode(values, False, check_zero)
+
+
+def encode_ternary(values: torch.Tensor) -> Planes:
+    """core.cpp:40-58 (plus plane, minus plane)."""
+    return _encode(values, True)
+
+
+def pack_b(b: Planes) -> PackedB:
+    """gemm.cpp:59-77: K x N planes (packed along N) -> PackedB panels."""
+    k, n = b.rows, b.cols
+    nbytes = int(L.lib.lowbit_packed_b_bytes(int(b.ternary), n, k))
+    panels = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=b.plane0.device)
+    L.check(L.lib.lowbit_pack_b(int(b.ternary), _ptr(b.plane0), _ptr(b.plane1), k, n, b.pitch, _ptr(panels),
+                                _stream()), "pack_b")
+    return PackedB(b.ternary, n, k, panels)
+
+
+def prepare_weights(pb: PackedB) -> Weights:
+    nbytes = int(L.lib.lowbit_weights_bytes(int(pb.ternary), pb.n, pb.k))
+    buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=pb.panels.device)
+    L.check(L.lib.lowbit_prepare_weights(int(pb.ternary), _ptr(pb.panels), pb.n, pb.k, _ptr(buf), _stream()),
+            "prepare_weights")
+    return Weights(pb.ternary, pb.n, pb.k, buf)
+
+
+def gemm_lowbit(mode: int, a: Planes, b: Union[PackedB, Weights], dims, k_blk: int = 4096,
+                kernel: int = KERNEL_AUTO, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """gemm.cpp:79-112.  dims = (m, n, k) (GemmDims).  Returns int16 [m, n]."""
+    m, n, k = dims
+    w = b if isinstance(b, Weights) else None
+    if out is None:
+        out = torch.empty((max(m, 1), max(n, 1)), dtype=torch.int16, device=a.plane0.device)
+    if w is None and isinstance(b, PackedB):
+        # validate before preparing, so errors come out in the reference order
+        st = L.lib.lowbit_gemm(mode, _ptr(a.plane0), _ptr(a.plane1), a.pitch, a.rows, a.cols, None,
+                               int(b.ternary), b.n, b.k, m, n, k, k_blk, None, out.stride(0), kernel, _stream())
+        if st not in (L.OK, L.INVALID_ARGUMENT):
+            L.check(st, "gemm_lowbit")
+        w = prepare_weights(b)
+    L.check(L.lib.lowbit_gemm(mode, _ptr(a.plane0), _ptr(a.plane1), a.pitch, a.rows, a.cols, _ptr(w.buf),
+                              int(w.ternary), w.n, w.k, m, n, k, k_blk, _ptr(out), out.stride(0), kernel,
+                              _stream()), "gemm_lowbit")
+    return out
+
+
+def gemm_lowbit_host(mode: int, a0: np.ndarray, a1: Optional[np.ndarray], a_rows: int, a_cols: int,
+                     panels: np.ndarray, b_ternary: bool, b_n: int, b_k: int, dims, k_blk: int = 4096,
+                     kernel: int = KERNEL_AUTO, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Host buffers in, host int16 C out: one whole reference gemm_lowbit call
+    (upload, prepare B, run, download) through lowbit_gemm_lowbit_host."""
+    m, n, k = dims
+    if out is None:
+        out = np.empty((max(m, 1), max(n, 1)), np.int16)
+
+    def hp(x):
+        return C.c_void_p(x.ctypes.data) if x is not None else None
+
+    L.check(L.lib.lowbit_gemm_lowbit_host(mode, hp(a0), hp(a1), a_rows, a_cols, hp(panels), int(b_ternary), b_n,
+                                          b_k, m, n, k, k_blk, hp(out), kernel, _stream()), "gemm_lowbit")
+    return out
+
+
+def generate(dist: int, seed: int, matrix_id: int, rows: int, cols: int, row0: int = 0,
+             device="cuda") -> torch.Tensor:
+    """Counter-based synthetic {-1,0,+1} data, identical to oracle.generate."""
+    out = torch.empty((rows, cols), dtype=torch.int8, device=device)
+    L.check(L.lib.lowbit_generate(dist, seed, matrix_id, row0, rows, cols, _ptr(out), _stream()), "generate")
+    return out
+
+
+def select_kernel(mode: int, m: int, n: int, k: int) -> int:
+    return int(L.lib.lowbit_select_kernel(mode, m, n, k))

@@ -1,0 +1,212 @@
+// capi.cu — the C-ABI surface (include/lowbit_cuda.h): argument validation in
+// the reference's order, kernel choice, and the host-buffer drop-in entry.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "layout.cuh"
+
+namespace lb {
+lowbit_status launch_bitserial(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+                               int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                               cudaStream_t stream);
+lowbit_status launch_tensor(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+                            int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                            cudaStream_t stream);
+}  // namespace lb
+
+namespace {
+thread_local std::string g_msg;
+thread_local long long g_v0 = 0, g_v1 = 0;
+}  // namespace
+
+namespace lbhost {
+lowbit_status set_error(lowbit_status st, const char* msg, long long v0, long long v1) {
+    g_msg = msg ? msg : "";
+    g_v0 = v0;
+    g_v1 = v1;
+    return st;
+}
+lowbit_status cuda_status(cudaError_t e, const char* where) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), where);
+    return set_error(LOWBIT_CUDA_ERROR, buf);
+}
+}  // namespace lbhost
+
+using lbhost::set_error;
+
+extern "C" int lowbit_abi_version(void) { return LOWBIT_ABI_VERSION; }
+
+extern "C" const char* lowbit_status_string(int st) {
+    switch (st) {
+        case LOWBIT_OK: return "OK";
+        case LOWBIT_ERROR: return "Error";
+        case LOWBIT_ZERO_IN_BINARY: return "ZeroInBinaryInput";
+        case LOWBIT_INVALID_CODE: return "InvalidCode";
+        case LOWBIT_OUT_OF_BOUNDS: return "OutOfBounds";
+        case LOWBIT_DEPTH_OVERFLOW: return "DepthOverflow";
+        case LOWBIT_MODE_MISMATCH: return "ModeMismatch";
+        case LOWBIT_CHANNEL_OVERFLOW: return "ChannelOverflow";
+        case LOWBIT_EMPTY_OUTPUT: return "EmptyOutput";
+        case LOWBIT_CUDA_ERROR: return "CudaError";
+        case LOWBIT_INVALID_ARGUMENT: return "InvalidArgument";
+        case LOWBIT_NO_DEVICE: return "NoDevice";
+        default: return "Unknown";
+    }
+}
+
+extern "C" const char* lowbit_last_error(void) { return g_msg.c_str(); }
+
+extern "C" void lowbit_last_error_values(long long* v0, long long* v1) {
+    if (v0) *v0 = g_v0;
+    if (v1) *v1 = g_v1;
+}
+
+extern "C" lowbit_status lowbit_device_check(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_error(LOWBIT_NO_DEVICE, "no CUDA device visible; liblowbit_cuda has no CPU fallback");
+    }
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major != 10) return set_error(LOWBIT_NO_DEVICE, "liblowbit_cuda is built for sm_100a only");
+    return LOWBIT_OK;
+}
+
+extern "C" long long lowbit_plane_pitch(int cols) {
+    long long b = (cols + 7) / 8;
+    return (b + 15) / 16 * 16;
+}
+
+// The reference's gemm_lowbit validation, in order (gemm.cpp:81-84, 94-100,
+// check_cfg gemm.cpp:9-12, check_dims gemm.cpp:14-19).
+static lowbit_status validate_gemm(int mode, bool a_ternary, int b_ternary, int a_rows, int a_cols, int b_n,
+                                   int b_k, int m, int n, int k, int k_blk) {
+    if (k_blk < 8 || (k_blk & 7) != 0) return set_error(LOWBIT_ERROR, "k_blk must be a positive multiple of 8");
+    if (mode < 0 || mode > 2) return set_error(LOWBIT_INVALID_ARGUMENT, "unknown gemm mode");
+    if (!a_ternary) {
+        if (mode != LOWBIT_BNN) return set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: binary left operand requires bnn mode");
+        if (b_ternary) return set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: bnn requires binary right operand");
+    } else {
+        if (mode == LOWBIT_BNN) return set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: bnn requires a binary left operand");
+        if (mode == LOWBIT_TNN && !b_ternary)
+            return set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: tnn requires a ternary right operand");
+        if (mode == LOWBIT_TBN && b_ternary)
+            return set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: tbn requires a binary right operand");
+    }
+    if (m <= 0 || n <= 0 || k <= 0) return set_error(LOWBIT_OUT_OF_BOUNDS, "out of bounds: gemm dims");
+    if (a_rows != m || a_cols != k) return set_error(LOWBIT_OUT_OF_BOUNDS, "out of bounds: left operand shape");
+    if (b_k != k || b_n != n) return set_error(LOWBIT_OUT_OF_BOUNDS, "out of bounds: packed right operand shape");
+    if (k > LOWBIT_K_MAX16) {
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "depth %d exceeds k_max %d", k, LOWBIT_K_MAX16);
+        return set_error(LOWBIT_DEPTH_OVERFLOW, buf, k, LOWBIT_K_MAX16);
+    }
+    return LOWBIT_OK;
+}
+
+// Static per-shape kernel table.  Measured on B200:
+// the tcgen05 path wins every shape whose tile grid fills the machine; the
+// bit-serial path is kept for tiny / launch-bound shapes.
+extern "C" int lowbit_select_kernel(int mode, int m, int n, int k) {
+    (void)mode;
+    const double ops = 2.0 * m * (double)n * k;
+    if (ops < 2.0e8 && m < 512) return LOWBIT_KERNEL_BITSERIAL;
+    return LOWBIT_KERNEL_TENSOR;
+}
+
+extern "C" lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int a_rows,
+                                     int a_cols, const void* weights, int b_ternary, int b_n, int b_k, int m, int n,
+                                     int k, int k_blk, int16_t* c, long long ldc, int kernel, lowbit_stream stream) {
+    const bool a_ternary = a1 != nullptr;
+    lowbit_status st = validate_gemm(mode, a_ternary, b_ternary, a_rows, a_cols, b_n, b_k, m, n, k, k_blk);
+    if (st) return st;
+    if (!a0 || !weights || !c) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: NULL pointer");
+    if ((a_pitch & 15) || a_pitch < (k + 7) / 8 || (reinterpret_cast<uintptr_t>(a0) & 15) ||
+        (a_ternary && (reinterpret_cast<uintptr_t>(a1) & 15)))
+        return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: A planes need 16-byte aligned rows (pitch % 16 == 0)");
+    if ((reinterpret_cast<uintptr_t>(weights) & 255))
+        return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: weights must be 256-byte aligned");
+    if (ldc < n) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: ldc < n");
+    if (kernel == LOWBIT_KERNEL_AUTO) kernel = lowbit_select_kernel(mode, m, n, k);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (kernel == LOWBIT_KERNEL_BITSERIAL)
+        return lb::launch_bitserial(mode, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    if (kernel == LOWBIT_KERNEL_TENSOR)
+        return lb::launch_tensor(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown kernel id");
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer drop-in.  Per-thread grow-only device scratch.
+// ---------------------------------------------------------------------------
+namespace {
+struct Scratch {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        want = (want + 0xFFFFF) & ~size_t(0xFFFFF);
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+};
+struct HostCtx {
+    Scratch a0, a1, panels, weights, c;
+};
+thread_local HostCtx g_ctx;
+}  // namespace
+
+extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t* a1, int a_rows,
+                                                 int a_cols, const uint8_t* panels, int b_ternary, int b_n, int b_k,
+                                                 int m, int n, int k, int k_blk, int16_t* c, int kernel,
+                                                 lowbit_stream stream) {
+    const bool a_ternary = a1 != nullptr;
+    lowbit_status st = validate_gemm(mode, a_ternary, b_ternary, a_rows, a_cols, b_n, b_k, m, n, k, k_blk);
+    if (st) return st;
+    if (!a0 || !panels || !c) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm_lowbit_host: NULL pointer");
+    if ((st = lowbit_device_check())) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long hstride = (k + 7) / 8;
+    const long long pitch = lowbit_plane_pitch(k);
+    const size_t abytes = (size_t)m * pitch;
+    const size_t pbytes = lowbit_packed_b_bytes(b_ternary, n, k);
+    const size_t wbytes = lowbit_weights_bytes(b_ternary, n, k);
+    HostCtx& X = g_ctx;
+    LB_CUDA_TRY(X.a0.ensure(abytes));
+    if (a_ternary) LB_CUDA_TRY(X.a1.ensure(abytes));
+    LB_CUDA_TRY(X.panels.ensure(pbytes));
+    LB_CUDA_TRY(X.weights.ensure(wbytes));
+    LB_CUDA_TRY(X.c.ensure((size_t)m * n * sizeof(int16_t)));
+    if (pitch == hstride) {
+        LB_CUDA_TRY(cudaMemcpyAsync(X.a0.ptr, a0, abytes, cudaMemcpyHostToDevice, s));
+        if (a_ternary) LB_CUDA_TRY(cudaMemcpyAsync(X.a1.ptr, a1, abytes, cudaMemcpyHostToDevice, s));
+    } else {  // re-pitch to 16-byte rows; zero the padding first
+        LB_CUDA_TRY(cudaMemsetAsync(X.a0.ptr, 0, abytes, s));
+        LB_CUDA_TRY(cudaMemcpy2DAsync(X.a0.ptr, pitch, a0, hstride, hstride, m, cudaMemcpyHostToDevice, s));
+        if (a_ternary) {
+            LB_CUDA_TRY(cudaMemsetAsync(X.a1.ptr, 0, abytes, s));
+            LB_CUDA_TRY(cudaMemcpy2DAsync(X.a1.ptr, pitch, a1, hstride, hstride, m, cudaMemcpyHostToDevice, s));
+        }
+    }
+    LB_CUDA_TRY(cudaMemcpyAsync(X.panels.ptr, panels, pbytes, cudaMemcpyHostToDevice, s));
+    if ((st = lowbit_prepare_weights(b_ternary, static_cast<const uint8_t*>(X.panels.ptr), n, k, X.weights.ptr,
+                                     stream)))
+        return st;
+    if ((st = lowbit_gemm(mode, static_cast<const uint8_t*>(X.a0.ptr),
+                          a_ternary ? static_cast<const uint8_t*>(X.a1.ptr) : nullptr, pitch, a_rows, a_cols,
+                          X.weights.ptr, b_ternary, b_n, b_k, m, n, k, k_blk, static_cast<int16_t*>(X.c.ptr), n,
+                          kernel, stream)))
+        return st;
+    LB_CUDA_TRY(cudaMemcpyAsync(c, X.c.ptr, (size_t)m * n * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
+    LB_CUDA_TRY(cudaStreamSynchronize(s));
+    return LOWBIT_OK;
+}

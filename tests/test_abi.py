@@ -1,0 +1,83 @@
+"""CPU: the C-ABI library loads, exports every symbol include/lowbit_cuda.h
+declares, and reports the reference's error contract in the reference's order
+(validation runs before any device work, so it is checkable without a GPU)."""
+import ctypes as C
+import re
+
+import pytest
+
+import paper_2205_09120_b200 as lb
+from paper_2205_09120_b200 import _lib as L
+
+
+def declared_symbols():
+    text = open(L.HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(lowbit_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L.lib, s), s
+        assert s in L.SIGNATURES, f"{s} missing from the ctypes signature table"
+
+
+def test_abi_version_and_strings():
+    assert L.lib.lowbit_abi_version() == 1
+    names = [L.lib.lowbit_status_string(i).decode() for i in range(12)]
+    assert names[:9] == ["OK", "Error", "ZeroInBinaryInput", "InvalidCode", "OutOfBounds", "DepthOverflow",
+                         "ModeMismatch", "ChannelOverflow", "EmptyOutput"]
+
+
+def test_layout_helpers():
+    assert [L.lib.lowbit_plane_pitch(c) for c in (1, 8, 9, 128, 129, 256, 2048)] == [16, 16, 16, 16, 32, 32, 256]
+    # PackedB bytes: ceil(n/8) panels x group x ceil(k/8) (pack.cpp:36-44, gemm.cpp:59-77)
+    assert L.lib.lowbit_packed_b_bytes(0, 8192, 4096) == 1024 * 8 * 512
+    assert L.lib.lowbit_packed_b_bytes(1, 96, 256) == 12 * 16 * 32
+    assert L.lib.lowbit_packed_b_bytes(1, 9, 17) == 2 * 16 * 3
+    assert L.lib.lowbit_weights_bytes(1, 96, 256) > 0
+
+
+def gemm_status(mode, a_ternary, b_ternary, a_rows, a_cols, b_n, b_k, m, n, k, k_blk=4096):
+    a1 = C.c_void_p(16) if a_ternary else None  # never dereferenced: validation fails first
+    return L.lib.lowbit_gemm(mode, C.c_void_p(16), a1, 16, a_rows, a_cols, None, b_ternary, b_n, b_k, m, n, k,
+                             k_blk, None, n, 0, None)
+
+
+def test_validation_order_matches_reference():
+    # check_cfg first (gemm.cpp:9-12), even with a mode mismatch present
+    assert gemm_status(L.TNN, 0, 0, 4, 4, 4, 4, 4, 4, 4, k_blk=7) == L.ERROR
+    assert gemm_status(L.BNN, 0, 0, 4, 4, 4, 4, 4, 4, 4, k_blk=0) == L.ERROR
+    # mode before dims (gemm.cpp:81-84, 94-99)
+    assert gemm_status(L.TNN, 0, 1, 4, 4, 4, 4, 0, 0, 0) == L.MODE_MISMATCH   # binary A needs bnn
+    assert gemm_status(L.BNN, 0, 1, 4, 4, 4, 4, 4, 4, 4) == L.MODE_MISMATCH   # bnn needs binary B
+    assert gemm_status(L.BNN, 1, 0, 4, 4, 4, 4, 4, 4, 4) == L.MODE_MISMATCH   # bnn needs binary A
+    assert gemm_status(L.TNN, 1, 0, 4, 4, 4, 4, 4, 4, 4) == L.MODE_MISMATCH   # tnn needs ternary B
+    assert gemm_status(L.TBN, 1, 1, 4, 4, 4, 4, 4, 4, 4) == L.MODE_MISMATCH   # tbn needs binary B
+    # check_dims (gemm.cpp:14-19)
+    assert gemm_status(L.TNN, 1, 1, 4, 4, 4, 4, 0, 4, 4) == L.OUT_OF_BOUNDS
+    assert gemm_status(L.TNN, 1, 1, 5, 4, 4, 4, 4, 4, 4) == L.OUT_OF_BOUNDS
+    assert gemm_status(L.TNN, 1, 1, 4, 4, 3, 4, 4, 4, 4) == L.OUT_OF_BOUNDS
+    assert gemm_status(L.BNN, 0, 0, 16, 32768, 8, 32768, 16, 8, 32768) == L.DEPTH_OVERFLOW
+    v0, v1 = C.c_longlong(), C.c_longlong()
+    L.lib.lowbit_last_error_values(C.byref(v0), C.byref(v1))
+    assert (v0.value, v1.value) == (32768, 32767)
+    assert L.lib.lowbit_last_error().decode() == "depth 32768 exceeds k_max 32767"  # errors.hpp:24-27
+    # passes validation -> stops at the NULL device pointers, not in a kernel
+    assert gemm_status(L.BNN, 0, 0, 16, 32767, 8, 32767, 16, 8, 32767) == L.INVALID_ARGUMENT
+
+
+def test_exceptions_map_to_reference_types():
+    with pytest.raises(lb.DepthOverflow) as e:
+        L.check(gemm_status(L.BNN, 0, 0, 16, 40000, 8, 40000, 16, 8, 40000))
+    assert e.value.k == 40000 and e.value.k_max == 32767
+    with pytest.raises(lb.ModeMismatch):
+        L.check(gemm_status(L.TNN, 1, 0, 4, 4, 4, 4, 4, 4, 4))
+    assert issubclass(lb.ZeroInBinaryInput, lb.Error) and issubclass(lb.NoDevice, lb.Error)
+
+
+def test_select_kernel_table():
+    assert L.lib.lowbit_select_kernel(L.TNN, 1048576, 1024, 2048) == L.KERNEL_TENSOR
+    assert L.lib.lowbit_select_kernel(L.BNN, 8192, 8192, 4096) == L.KERNEL_TENSOR
+    assert L.lib.lowbit_select_kernel(L.TBN, 72, 24, 128) in (L.KERNEL_BITSERIAL, L.KERNEL_TENSOR)
