@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""bench.py — low-bit GeMM throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (default, BASELINE.json configs[4] = "c5"): TNN GeMM, A = 1,048,576 x
+2048 ternary (P(0)=1/3), B = 2048 x 1024 ternary, int16 C; A rows sharded
+contiguously over the N ranks, B replicated (weights: encoded + pack_b +
+prepared once, untimed, as the reference bench does, bench.cpp:40-68).
+Total work is fixed as N grows -> "scaling": "strong".  No collective on the
+data path (north_star: NCCL only gathers outputs where a test requires it).
+
+One step = one gemm_lowbit over this rank's rows with the encoded A planes
+resident in HBM (the reference timing policy: encode and pack_b excluded,
+bench.cpp:49,58).  L2 is flushed (256 MiB write) between steps, outside the
+CUDA events that time each step's kernel.  value = 2*M*N*K / max-over-ranks of
+the per-step device time, in TOPS.
+
+e2e: the same metric through the reference-facing host call
+(lowbit_gemm_lowbit_host: host A planes + host PackedB in, host int16 C out),
+pinned host buffers, copies inside the timed region.
+
+cpu_baseline / --impl reference: the reference library itself
+(oracle/_ref/liblowbit_ref.so, built from /root/reference/proj/src with its
+own flags) on a bounded row sample of the same workload, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (mode, M, N, K, dist_a, dist_b, seed)   modes: 0 bnn, 1 tnn, 2 tbn
+    "c1": (1, 360, 96, 256, 0, 0, 43),
+    "c3": (0, 8192, 8192, 4096, 1, 1, 45),
+    "c5": (1, 1048576, 1024, 2048, 0, 0, 47),
+}
+MODE_NAME = {0: "bnn", 1: "tnn", 2: "tbn"}
+SWEEP = [(m, n, k) for m in (72, 120, 240, 360) for n in (24, 48, 72, 96) for k in (128, 256, 384, 512)]
+
+
+def peaks():
+    p = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+    except OSError:
+        pass
+    return {
+        "hbm_gbs": p.get("hbm_gbs", 6650.0),
+        "bf16_tflops": p.get("bf16_tflops", 1590.0),
+        "bf16_tflops_sustained": p.get("bf16_tflops_sustained", 1400.0),
+        "source": "measured (MEASURED_PEAKS.json)" if p else "fallback (B200_PROFILING.md)",
+        "sm_max_mhz": p.get("sm_max_mhz", 1965.0),
+    }
+
+
+class ClockSampler:
+    """Clocks + throttle reasons sampled during the timed region (NVML every
+    5 ms; nvidia-smi -lms 100 as a fallback)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.stop = False
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _poll(self):
+        nv = self.nvml
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4}
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                act = ["Active" if r & bit else "Not Active" for bit in names.values()]
+                self.lines.append(", ".join([str(sm), str(mx), "0"] + act))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop = True
+            self.t.join(timeout=1)
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref) on a bounded sample
+# ---------------------------------------------------------------------------
+def reference_cpu_rate(cfg_name, target_s=8.0, threads=None):
+    from oracle.oracle import Port, Ref, a_mode_ternary, b_mode_ternary
+    mode, M, N, K, da, db, seed = CONFIGS[cfg_name]
+    port = Port()
+    kind = "reference" if Ref.available() else "port"
+    if kind != "reference":
+        return None
+    ref = Ref()
+    threads = threads or os.cpu_count() or 1
+    b = port.generate(db, seed, 1, K, N)
+    b0, b1 = ref.encode(b, b_mode_ternary(mode))
+
+    def run(rows, reps=1):
+        rows = min(rows, M)
+        a = port.generate(da, seed, 0, rows, K)
+        a0, a1 = ref.encode(a, a_mode_ternary(mode))
+        h = ref.bench_prepare(mode, a0, a1, rows, K, b0, b1, N, threads)
+        ref.bench_run(h)  # warm-up (bench.cpp:214)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ref.bench_run(h)
+            ts.append(time.perf_counter() - t0)
+        ref.bench_free(h)
+        return rows, float(np.median(ts))
+
+    rows, t = run(max(threads, 16))
+    while t < 0.5 and rows < M:  # calibrate: thread start-up dominates tiny samples
+        rows, t = run(min(M, rows * 4))
+    ops_rate = 2.0 * rows * N * K / t
+    rows = int(min(M, max(rows, target_s * ops_rate / (2.0 * N * K))))
+    rows, t = run(rows)
+    return {"value": 2.0 * rows * N * K / t / 1e12, "unit": "TOPS", "cores": threads, "kind": kind,
+            "sample": f"{MODE_NAME[mode]} {rows} x {N} x {K} rows of {cfg_name} (gemm_lowbit on {threads} "
+                      f"row shards, encode/pack_b excluded, median after warm-up), {t:.2f} s",
+            "seconds": t}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    mode, M, N, K, da, db, seed = CONFIGS[args.config]
+    from oracle.oracle import Ref
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblowbit_ref.so not built"}))
+        return
+    per_step = max(1.0, min(8.0, 60.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    r = None
+    for i in range(args.warmup + args.steps):
+        r = reference_cpu_rate(args.config, target_s=per_step)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = float(np.mean(vals))
+    ops = 2.0 * M * N * K
+    line = {
+        "impl": "reference", "metric": f"low-bit GeMM TOPS (MAC=2 ops), {MODE_NAME[mode]} {args.config}",
+        "value": v, "unit": "TOPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ops / (v * 1e12) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8 bit-planes / int16", "data": "synthetic (counter-based generator)",
+        "config": {"workload": f"{args.config}: {MODE_NAME[mode]} M={M} N={N} K={K}, reference CPU path "
+                               f"extrapolated from a bounded row sample per step"},
+        "cpu_baseline": {"value": v, "unit": "TOPS", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]},
+        "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "bitserial"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-config side measurements")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_09120_b200 as lb
+    from paper_2205_09120_b200 import _lib as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    kernel = {"auto": lb.KERNEL_AUTO, "tensor": lb.KERNEL_TENSOR, "bitserial": lb.KERNEL_BITSERIAL}[args.kernel]
+
+    mode, M, N, K, da, db, seed = CONFIGS[args.config]
+    r0 = M * rank // world
+    r1 = M * (rank + 1) // world
+    m = r1 - r0
+
+    # ---- untimed setup: inputs in HBM, weights prepared ----
+    a = lb.generate(da, seed, 0, m, K, row0=r0)
+    ap_ = lb.encode_binary(a) if mode == 0 else lb.encode_ternary(a)
+    del a
+    b = lb.generate(db, seed, 1, K, N)
+    bp = lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)
+    pb = lb.pack_b(bp)
+    w = lb.prepare_weights(pb)
+    c = torch.empty((m, N), dtype=torch.int16, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    chosen = kernel if kernel else lb.select_kernel(mode, m, N, K)
+
+    def step():
+        lb.gemm_lowbit(mode, ap_, w, (m, N, K), kernel=kernel, out=c)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    my_ms = float(np.sum(step_ms))
+    t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    ops_total = 2.0 * M * N * K
+    value = ops_total / (ms_per_step * 1e-3) / 1e12
+    kernel_ms_avg = my_ms / args.steps
+    ops_rank = 2.0 * m * N * K
+
+    # ---- e2e through the reference-facing host call ----
+    e2e = None
+    if not args.no_e2e:
+        sb = (K + 7) // 8
+        h_a0 = torch.empty((m, sb), dtype=torch.uint8, pin_memory=True)
+        h_a0.copy_(ap_.plane0[:, :sb])
+        h_a1 = None
+        if ap_.plane1 is not None:
+            h_a1 = torch.empty((m, sb), dtype=torch.uint8, pin_memory=True)
+            h_a1.copy_(ap_.plane1[:, :sb])
+        h_pan = torch.empty(pb.panels.numel(), dtype=torch.uint8, pin_memory=True)
+        h_pan.copy_(pb.panels)
+        h_c = torch.empty((m, N), dtype=torch.int16, pin_memory=True)
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+        def e2e_step():
+            L.check(L.lib.lowbit_gemm_lowbit_host(
+                mode, C.c_void_p(h_a0.data_ptr()), C.c_void_p(h_a1.data_ptr()) if h_a1 is not None else None,
+                m, K, C.c_void_p(h_pan.data_ptr()), int(mode == 1), N, K, m, N, K, 4096,
+                C.c_void_p(h_c.data_ptr()), kernel, stream), "e2e")
+
+        e2e_steps = max(2, min(args.steps, 5))
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es.record()
+        for _ in range(e2e_steps):
+            e2e_step()
+        ee.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([es.elapsed_time(ee) / e2e_steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = h_a0.numel() + (h_a1.numel() if h_a1 is not None else 0) + h_pan.numel()
+        e2e = {"value": ops_total / (te.item() * 1e-3) / 1e12, "unit": "TOPS",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h_c.numel() * 2),
+               "ms_per_step": te.item(), "path": "lowbit_gemm_lowbit_host (pinned host planes + PackedB in, "
+                                                 "int16 C out; includes B upload + prepare per call)"}
+        # sanity: e2e output equals the device-resident output
+        assert torch.equal(h_c.cuda(), c), "e2e output differs from device path"
+        del h_a0, h_a1, h_c
+
+    pk = peaks()
+    tensor_peak = 2.0 * pk["bf16_tflops"]  # dense int8 tcgen05 = 2x bf16 per SM-clock (4.5 vs 2.25 PF spec)
+    achieved = ops_rank / (kernel_ms_avg * 1e-3) / 1e12
+    traffic = load_traffic().get(f"{args.config}:{'tensor' if chosen == lb.KERNEL_TENSOR else 'bitserial'}")
+    if chosen == lb.KERNEL_TENSOR:
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TOP/s",
+                "frac": achieved / tensor_peak, "traffic": traffic,
+                "kernel": "gemm_tc_kernel (tcgen05.mma kind::i8)",
+                "peak_source": f"2 x bf16 dense {pk['bf16_tflops']} TFLOP/s, {pk['source']}",
+                "algorithmic_ops_per_launch": ops_rank}
+    else:
+        popc_peak = 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
+        roof = {"bound": "popc", "achieved": achieved, "peak": popc_peak, "unit": "TOP/s",
+                "frac": achieved / popc_peak, "traffic": traffic, "kernel": "gemm_bitserial_kernel",
+                "peak_source": "148 SMs x 16 POPC/clk x 32 bits x 2 ops x max clock (TNN: 2 POPC per word)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = reference_cpu_rate(args.config)
+        except Exception as e:  # never let the baseline break the bench line
+            cpu = {"value": None, "error": str(e)}
+
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = side_configs(lb, torch, flush, pk)
+
+    if rank == 0:
+        line = {
+            "metric": f"low-bit GeMM TOPS (MAC=2 ops), {MODE_NAME[mode]} {args.config}",
+            "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8 bit-planes in, int8 tensor-core MMA, int32 accumulate, int16 out",
+            "data": "synthetic (counter-based splitmix64 generator, BASELINE.json distributions)",
+            "config": {"workload": f"{args.config}: {MODE_NAME[mode]} GeMM M={M} N={N} K={K} int16 C, "
+                                   f"A rows sharded over {world} GPU(s), B replicated",
+                       "global_rows": M, "rows_per_rank": M // world, "l2": "flushed (256 MiB write) between steps",
+                       "kernel": {1: "bitserial", 2: "tensor"}.get(chosen, str(chosen)),
+                       "parallelism": f"row-shard x{world}"},
+            "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "per_config": extra,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def time_device(torch, fn, flush, reps=10):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return float(np.median(ts))
+
+
+def side_configs(lb, torch, flush, pk):
+    """Configs 1-3 at N=1 (both kernels where meaningful): latency and TOPS."""
+    out = {}
+    tensor_peak = 2.0 * pk["bf16_tflops"]
+    for name in ("c1", "c3"):
+        mode, M, N, K, da, db, seed = CONFIGS[name]
+        a = lb.generate(da, seed, 0, M, K)
+        ap_ = lb.encode_binary(a) if mode == 0 else lb.encode_ternary(a)
+        b = lb.generate(db, seed, 1, K, N)
+        w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)))
+        c = torch.empty((M, N), dtype=torch.int16, device="cuda")
+        res = {}
+        for kn, kid in (("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL)):
+            ms = time_device(torch, lambda: lb.gemm_lowbit(mode, ap_, w, (M, N, K), kernel=kid, out=c), flush)
+            tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
+            res[kn] = {"ms": ms, "TOPS": tops}
+        res["tensor"]["frac_of_tensor_peak"] = res["tensor"]["TOPS"] / tensor_peak
+        popc_peak = 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
+        res["bitserial"]["frac_of_popc_peak"] = res["bitserial"]["TOPS"] / popc_peak
+        res["auto"] = {1: "bitserial", 2: "tensor"}[lb.select_kernel(mode, M, N, K)]
+        out[name] = res
+    # c2: the 64-shape TBN sweep, one launch per shape, total device time
+    ws, aps, cs = [], [], []
+    for s, (M, N, K) in enumerate(SWEEP):
+        a = lb.generate(2, 44, 2 * s, M, K)
+        b = lb.generate(1, 44, 2 * s + 1, K, N)
+        aps.append(lb.encode_ternary(a))
+        ws.append(lb.prepare_weights(lb.pack_b(lb.encode_binary(b))))
+        cs.append(torch.empty((M, N), dtype=torch.int16, device="cuda"))
+    ops = sum(2.0 * M * N * K for M, N, K in SWEEP)
+    res = {}
+    for kn, kid in (("auto", lb.KERNEL_AUTO), ("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL)):
+        def sweep():
+            for s, (M, N, K) in enumerate(SWEEP):
+                lb.gemm_lowbit(2, aps[s], ws[s], (M, N, K), kernel=kid, out=cs[s])
+        ms = time_device(torch, sweep, flush, reps=5)
+        res[kn] = {"ms_total_64_shapes": ms, "TOPS": ops / (ms * 1e-3) / 1e12}
+    out["c2"] = res
+    return out
+
+
+if __name__ == "__main__":
+    main()

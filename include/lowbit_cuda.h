@@ -62,8 +62,10 @@ typedef enum lowbit_gemm_mode { LOWBIT_BNN = 0, LOWBIT_TNN = 1, LOWBIT_TBN = 2 }
  * (lowbit_select_kernel); the others force one kernel (tests, profiling). */
 typedef enum lowbit_kernel {
     LOWBIT_KERNEL_AUTO = 0,
-    LOWBIT_KERNEL_BITSERIAL = 1, /* K2: LOP3 + POPC, int32 registers */
-    LOWBIT_KERNEL_TENSOR = 2     /* K3: tcgen05.mma kind::i8, int32 TMEM accumulators */
+    LOWBIT_KERNEL_BITSERIAL = 1,  /* K2: LOP3 + POPC, int32 registers */
+    LOWBIT_KERNEL_TENSOR = 2,     /* K3: tcgen05.mma kind::i8, int32 TMEM accumulators; CTA pairs
+                                     (cta_group::2, 256-row tiles) when m > 128, else one CTA */
+    LOWBIT_KERNEL_TENSOR_1CTA = 3 /* K3 forced to the single-CTA (cta_group::1) variant */
 } lowbit_kernel;
 
 typedef void* lowbit_stream; /* cudaStream_t */

@@ -11,6 +11,9 @@ namespace lb {
 lowbit_status launch_bitserial(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                                int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                                cudaStream_t stream);
+lowbit_status launch_tensor_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m,
+                                 int n, int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                                 cudaStream_t stream);
 lowbit_status launch_tensor(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                             int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                             cudaStream_t stream);
@@ -136,7 +139,9 @@ extern "C" lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t*
     cudaStream_t s = (cudaStream_t)stream;
     if (kernel == LOWBIT_KERNEL_BITSERIAL)
         return lb::launch_bitserial(mode, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
-    if (kernel == LOWBIT_KERNEL_TENSOR)
+    if (kernel == LOWBIT_KERNEL_TENSOR && m > 128)
+        return lb::launch_tensor_pair(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    if (kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_1CTA)
         return lb::launch_tensor(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown kernel id");
 }

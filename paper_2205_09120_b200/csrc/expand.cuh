@@ -1,0 +1,47 @@
+// expand.cuh — bit planes -> int8 UMMA operand rows (converter warps of K3).
+#pragma once
+#include "common.cuh"
+
+namespace lb {
+
+// One converter thread: A row r, raw bytes [8h, 8h+8) of the row's 16-byte
+// k-block chunk (64 elements) -> int8 UMMA chunks 4h..4h+3 (16 B each) of the
+// K-major 128B-swizzled tile.  ~2 integer ops per element:
+//   nibble isolate (PRMT) -> spread4 (IMAD+LOP) -> minus*0xFF + plus (IMAD).
+template <bool A_TER>
+__device__ __forceinline__ void expand_half(uint32_t raw_p, uint32_t raw_m, uint32_t a_tile, int r, int h) {
+    const uint2 p = lds_v2(raw_p + r * 16 + 8 * h);
+    uint2 m = make_uint2(0, 0);
+    if (A_TER) m = lds_v2(raw_m + r * 16 + 8 * h);
+    const uint32_t row = a_tile + r * 128;
+    const int sw = r & 7;
+#pragma unroll
+    for (int wi = 0; wi < 2; ++wi) {
+        const uint32_t pw = wi ? p.y : p.x, mw = wi ? m.y : m.x;
+        const uint32_t p_lo = pw & 0x0F0F0F0Fu, p_hi = (pw >> 4) & 0x0F0F0F0Fu;
+        const uint32_t m_lo = mw & 0x0F0F0F0Fu, m_hi = (mw >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t w[4];
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb) {
+                const uint32_t sel = 0x4440u | (uint32_t)(2 * c + bb);
+                const uint32_t P0 = spread4(__byte_perm(p_lo, 0, sel));
+                const uint32_t P1 = spread4(__byte_perm(p_hi, 0, sel));
+                if (A_TER) {
+                    const uint32_t M0 = spread4(__byte_perm(m_lo, 0, sel));
+                    const uint32_t M1 = spread4(__byte_perm(m_hi, 0, sel));
+                    w[2 * bb] = M0 * 0xFFu + P0;  // +1 -> 0x01, -1 -> 0xFF, 0 -> 0x00 (disjoint planes)
+                    w[2 * bb + 1] = M1 * 0xFFu + P1;
+                } else {
+                    w[2 * bb] = (P0 * 0xFEu) ^ 0x01010101u;  // bit 1 -> 0xFF (-1), bit 0 -> 0x01 (+1)
+                    w[2 * bb + 1] = (P1 * 0xFEu) ^ 0x01010101u;
+                }
+            }
+            const int ch = 4 * h + 2 * wi + c;
+            sts_v4(row + ((ch ^ sw) << 4), w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+}  // namespace lb

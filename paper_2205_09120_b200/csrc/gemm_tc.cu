@@ -11,18 +11,18 @@
 //      int8 straight into the UMMA operand tile (K-major, 128-byte swizzle).
 //   B  the prepared int8 K-major weights (layout.cuh), TMA 128-byte swizzle.
 //
-// Warp roles (320 threads, 1 CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer (raw A bits + int8 B per 128-deep k-block)
-//   warp 1      TMEM allocator + single-thread UMMA issuer
-//   warps 2-5   converters: one A row each, bits -> int8, swizzled STS
-//   warps 6-9   epilogue: TMEM -> registers -> int16 -> global
+// Warp roles (448 threads, 1 CTA per SM, persistent over output tiles):
+//   warp 0       TMA producer (raw A bits + int8 B per 128-deep k-block)
+//   warp 1       TMEM allocator + single-thread UMMA issuer
+//   warps 2-9    converters: half an A row each, bits -> int8, swizzled STS
+//   warps 10-13  epilogue: TMEM -> registers -> int16 -> global
 // Pipelines: STAGES-deep smem ring (tma_full / a_ready / empty), and a
 // double-buffered TMEM accumulator (2 x 256 columns; tmem_full / tmem_empty)
 // so the epilogue of tile t overlaps the MMAs of tile t+1.
-#include <cudaTypedefs.h>
-
 #include "common.cuh"
+#include "expand.cuh"
 #include "layout.cuh"
+#include "tmap.cuh"
 
 namespace lb {
 
@@ -30,7 +30,7 @@ constexpr int TC_BM = 128;         // UMMA M (rows of A per tile)
 constexpr int TC_BK = 128;         // depth per k-block (bytes of int8 = one 128B swizzle row)
 constexpr int TC_MAX_BN = 256;     // UMMA N max
 constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 320;
+constexpr int TC_THREADS = 448;  // 2 control + 8 converter + 4 epilogue warps
 constexpr int TC_A_BYTES = TC_BM * TC_BK;           // 16 KB
 constexpr int TC_B_BYTES = TC_MAX_BN * TC_BK;       // 32 KB
 constexpr int TC_RAW_BYTES = TC_BM * 16;            // one plane, 128 rows x 16 B
@@ -41,34 +41,6 @@ struct TcParams {
     long long ldc;
     int16_t* c;
 };
-
-template <bool A_TER>
-__device__ __forceinline__ void expand_row(const uint8_t* raw_p, const uint8_t* raw_m, uint8_t* a_tile, int r) {
-    const uint4 p4 = *reinterpret_cast<const uint4*>(raw_p + r * 16);
-    uint4 m4 = make_uint4(0, 0, 0, 0);
-    if (A_TER) m4 = *reinterpret_cast<const uint4*>(raw_m + r * 16);
-    const uint32_t pw[4] = {p4.x, p4.y, p4.z, p4.w};
-    const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
-    uint8_t* row = a_tile + r * 128;
-    const int sw = r & 7;
-#pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-        const uint32_t p16 = (pw[ch >> 1] >> ((ch & 1) * 16)) & 0xFFFFu;
-        const uint32_t m16 = (mw[ch >> 1] >> ((ch & 1) * 16)) & 0xFFFFu;
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t pb = spread4((p16 >> (4 * q)) & 0xFu);
-            if (A_TER) {
-                const uint32_t mb = spread4((m16 >> (4 * q)) & 0xFu);
-                w[q] = pb | (mb * 0xFFu);  // +1 -> 0x01, -1 -> 0xFF, 0 -> 0x00
-            } else {
-                w[q] = (pb * 0xFEu) ^ 0x01010101u;  // bit 1 -> 0xFF (-1), bit 0 -> 0x01 (+1)
-            }
-        }
-        *reinterpret_cast<uint4*>(row + ((ch ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-}
 
 template <bool A_TER>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -95,7 +67,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&tma_full[s], 1);
-            mbar_init(&a_ready[s], 4);
+            mbar_init(&a_ready[s], 8);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -166,16 +138,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-    } else if (warp < 6) {
+    } else if (warp < 10) {
         // ===================== converters =====================
-        const int r = threadIdx.x - 64;  // A row within the tile
+        const int ct = threadIdx.x - 64;
+        const int r = ct & 127, h = ct >> 7;  // A row within the tile, half of its 16 raw bytes
+        const uint32_t sA_u = smem_u32(sA), sRaw_u = smem_u32(sRaw);
         int stage = 0;
         uint32_t phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             for (int kb = 0; kb < prm.kblocks; ++kb) {
                 mbar_wait(&tma_full[stage], phase);
-                const uint8_t* raw = sRaw + stage * 2 * TC_RAW_BYTES;
-                expand_row<A_TER>(raw, raw + TC_RAW_BYTES, sA + stage * TC_A_BYTES, r);
+                const uint32_t raw = sRaw_u + stage * 2 * TC_RAW_BYTES;
+                expand_half<A_TER>(raw, raw + TC_RAW_BYTES, sA_u + stage * TC_A_BYTES, r, h);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_ready[stage]);
@@ -232,43 +206,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-static bool make_map_2d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1, uint64_t stride1,
-                        uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
-    auto fn = get_encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {dim0, dim1};
-    cuuint64_t strides[1] = {stride1};
-    cuuint32_t box[2] = {box0, box1};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-static int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
 // Tile width along N: one UMMA of N = bn (multiple of 32, <= 256).
 static int pick_bn(int n) {
     if (n >= 256) return 256;

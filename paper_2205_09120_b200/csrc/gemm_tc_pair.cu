@@ -1,0 +1,321 @@
+// gemm_tc_pair.cu — K3 in CTA-pair form: tcgen05.mma.cta_group::2 kind::i8.
+//
+// Same arithmetic as gemm_tc.cu (exact int8 contraction, int32 TMEM
+// accumulators, int16 out — bit-identical to gemm_lowbit, gemm.cpp:79-112),
+// re-tiled for the B200's two-SM tensor-core pairs:
+//
+//   * a cluster of 2 CTAs on one TPC computes a 256 x BN output tile
+//     (BN <= 256); CTA r owns A rows [128r, 128r+128) and B rows (output
+//     columns) [BN/2 r, BN/2 (r+1)) of the tile.  Each SM therefore streams
+//     only HALF of the B tile from L2 and reads half of it from shared
+//     memory — the B200 answer to this kernel's L2/SMEM bandwidth ceiling
+//     (profiles/r01: the 1-CTA kernel sat at the ~11.5 TB/s LTS cap).
+//   * the leader CTA (rank 0) issues every UMMA for the pair; the peer's
+//     converters and epilogue talk to the leader's mbarriers through
+//     shared::cluster addresses (mapa), and tcgen05.commit multicasts stage
+//     release / accumulator-ready to both CTAs.
+//   * the epilogue stages int16 sub-tiles in shared memory (64-byte swizzle)
+//     and writes them with TMA stores: full 32-byte sectors, no per-element
+//     bounds checks (TMA clips the ragged edges).
+//
+// Warp roles per CTA (448 threads): 0 TMA producer, 1 TMEM alloc + UMMA
+// issuer (leader only), 2-9 converters, 10-13 epilogue.
+#include "common.cuh"
+#include "expand.cuh"
+#include "layout.cuh"
+#include "tmap.cuh"
+
+namespace lb {
+
+constexpr int PR_BM = 128;          // A rows per CTA (256 per pair)
+constexpr int PR_BK = 128;          // depth per k-block
+constexpr int PR_MAX_BN = 256;      // pair UMMA N
+constexpr int PR_STAGES = 5;
+constexpr int PR_THREADS = 448;
+constexpr int PR_A_BYTES = PR_BM * PR_BK;              // 16 KB
+constexpr int PR_B_BYTES = (PR_MAX_BN / 2) * PR_BK;    // 16 KB (this CTA's half of B)
+constexpr int PR_RAW_BYTES = PR_BM * 16;               // one plane
+constexpr int PR_EPI_BYTES = 32 * 64;                  // 32 rows x 32 int16, per warp per buffer
+constexpr int PR_SMEM_BYTES =
+    1024 + PR_STAGES * (PR_A_BYTES + PR_B_BYTES + 2 * PR_RAW_BYTES) + 4 * 2 * PR_EPI_BYTES + 512;
+
+struct PairParams {
+    int m, n, kblocks, bn, m_tiles, n_tiles;
+    long long ldc;
+    int16_t* c;
+    int tma_store;
+};
+
+template <bool A_TER>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
+    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
+                        const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_c,
+                        const PairParams prm) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + PR_STAGES * PR_A_BYTES;
+    uint8_t* sRaw = sB + PR_STAGES * PR_B_BYTES;
+    uint8_t* sEpi = sRaw + PR_STAGES * 2 * PR_RAW_BYTES;  // 1024-aligned (all sizes are multiples of 1 KB)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * 2 * PR_EPI_BYTES);
+    uint64_t* raw_full = bars;                      // local: raw A bits landed
+    uint64_t* b_full = bars + PR_STAGES;            // leader: both halves of B landed
+    uint64_t* a_ready = bars + 2 * PR_STAGES;       // leader: 16 converter warps done
+    uint64_t* empty = bars + 3 * PR_STAGES;         // local: pair MMAs of this stage done
+    uint64_t* tmem_full = bars + 4 * PR_STAGES;     // local: accumulator ready (2)
+    uint64_t* tmem_empty = tmem_full + 2;           // leader: 8 epilogue warps drained (2)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int num_tiles = prm.m_tiles * prm.n_tiles;
+    const int bn = prm.bn, bnh = prm.bn >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < PR_STAGES; ++s) {
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&b_full[s], 1);
+            mbar_init(&a_ready[s], 16);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 8);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmap_b);
+        tma_prefetch_desc(&tmap_a0);
+        if (A_TER) tma_prefetch_desc(&tmap_a1);
+        if (prm.tma_store) tma_prefetch_desc(&tmap_c);
+    }
+    if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (lane == 0) {
+            const uint32_t raw_bytes = (A_TER ? 2 : 1) * PR_RAW_BYTES;
+            const uint32_t b_bytes_pair = (uint32_t)bn * PR_BK;  // both CTAs' halves
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
+                const int arow = mt * 2 * PR_BM + (int)rank * PR_BM;
+                const int brow = nt * bn + (int)rank * bnh;
+                for (int kb = 0; kb < prm.kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* raw = sRaw + stage * 2 * PR_RAW_BYTES;
+                    mbar_arrive_expect_tx(&raw_full[stage], raw_bytes);
+                    tma_load_2d(raw, &tmap_a0, &raw_full[stage], kb * 16, arow);
+                    if (A_TER) tma_load_2d(raw + PR_RAW_BYTES, &tmap_a1, &raw_full[stage], kb * 16, arow);
+                    if (leader) mbar_arrive_expect_tx(&b_full[stage], b_bytes_pair);
+                    tma_load_2d_pair(smem_u32(sB + stage * PR_B_BYTES), &tmap_b,
+                                     mapa_shared(smem_u32(&b_full[stage]), 0), kb * PR_BK, brow);
+                    if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== UMMA issuer (leader CTA only) =====================
+        if (leader) {
+            const uint32_t idesc = idesc_i8(2 * PR_BM, (uint32_t)bn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                mbar_wait_cluster(&tmem_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)acc * PR_MAX_BN;
+                for (int kb = 0; kb < prm.kblocks; ++kb) {
+                    mbar_wait_cluster(&a_ready[stage], phase);
+                    mbar_wait(&b_full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a_addr = smem_u32(sA + stage * PR_A_BYTES);
+                        const uint32_t b_addr = smem_u32(sB + stage * PR_B_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < PR_BK / 32; ++kk)
+                            umma_i8_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
+                                         umma_desc_k_sw128(b_addr + kk * 32), idesc, (kb | kk) != 0);
+                        umma_commit_pair(&empty[stage], 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (lane == 0) umma_commit_pair(&tmem_full[acc], 0x3);
+                __syncwarp();
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp < 10) {
+        // ===================== converters (both CTAs) =====================
+        const int ct = threadIdx.x - 64;
+        const int r = ct & 127, h = ct >> 7;
+        const uint32_t sA_u = smem_u32(sA), sRaw_u = smem_u32(sRaw);
+        const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = pair; tile < num_tiles; tile += npairs) {
+            for (int kb = 0; kb < prm.kblocks; ++kb) {
+                mbar_wait(&raw_full[stage], phase);
+                const uint32_t raw = sRaw_u + stage * 2 * PR_RAW_BYTES;
+                expand_half<A_TER>(raw, raw + PR_RAW_BYTES, sA_u + stage * PR_A_BYTES, r, h);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(a_ready0 + stage * 8);
+                if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue (both CTAs) =====================
+        const int wq = warp & 3;  // TMEM lane quarter
+        const int row_in_cta = wq * 32 + lane;
+        const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
+        const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 10) * 2 * PR_EPI_BYTES;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int nbuf = 0;
+        const bool vec_ok = ((prm.ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(prm.c) & 15) == 0);
+        for (int tile = pair; tile < num_tiles; tile += npairs) {
+            const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
+            const int row0 = mt * 2 * PR_BM + (int)rank * PR_BM + wq * 32;
+            mbar_wait(&tmem_full[acc], acc_phase);
+            tc_fence_after();
+            for (int ch = 0; ch < bn / 32; ++ch) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)acc * PR_MAX_BN + ch * 32, v);
+                tmem_ld_wait();
+                const int col0 = nt * bn + ch * 32;
+                if (prm.tma_store) {
+                    const uint32_t buf = epi + (uint32_t)nbuf * PR_EPI_BYTES;
+                    if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+                    __syncwarp();
+                    const uint32_t rowaddr = buf + lane * 64;
+                    const int sw = (lane >> 1) & 3;  // TMA SWIZZLE_64B: 16B chunk q -> q ^ ((row>>1)&3)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        sts_v4(rowaddr + ((q ^ sw) << 4), __byte_perm(v[8 * q + 0], v[8 * q + 1], 0x5410),
+                               __byte_perm(v[8 * q + 2], v[8 * q + 3], 0x5410),
+                               __byte_perm(v[8 * q + 4], v[8 * q + 5], 0x5410),
+                               __byte_perm(v[8 * q + 6], v[8 * q + 7], 0x5410));
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmap_c, buf, col0, row0);
+                        bulk_commit();
+                    }
+                    nbuf ^= 1;
+                } else {
+                    const int row = row0 + lane;
+                    if (row < prm.m) {
+                        int16_t* crow = prm.c + (long long)row * prm.ldc;
+                        if (vec_ok && col0 + 32 <= prm.n) {
+                            uint4* dst = reinterpret_cast<uint4*>(crow + col0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                dst[q] = make_uint4(__byte_perm(v[8 * q + 0], v[8 * q + 1], 0x5410),
+                                                    __byte_perm(v[8 * q + 2], v[8 * q + 3], 0x5410),
+                                                    __byte_perm(v[8 * q + 4], v[8 * q + 5], 0x5410),
+                                                    __byte_perm(v[8 * q + 6], v[8 * q + 7], 0x5410));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j < prm.n) crow[col0 + j] = (int16_t)(int32_t)v[j];
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (prm.tma_store && lane == 0) bulk_wait<0>();
+        (void)row_in_cta;
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<512>(tmem_base);
+    }
+}
+
+static int pick_bn_pair(int n) {
+    if (n >= 256) return 256;
+    int b = (n + 31) / 32 * 32;
+    return b < 64 ? 64 : b;
+}
+
+lowbit_status launch_tensor_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m,
+                                 int n, int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                                 cudaStream_t stream) {
+    const WeightsLayout L(b_ternary, n, k);
+    PairParams prm;
+    prm.m = m;
+    prm.n = n;
+    prm.kblocks = L.kp / PR_BK;
+    prm.bn = pick_bn_pair(n);
+    prm.m_tiles = (m + 2 * PR_BM - 1) / (2 * PR_BM);
+    prm.n_tiles = (n + prm.bn - 1) / prm.bn;
+    prm.ldc = ldc;
+    prm.c = c;
+    prm.tma_store = ((ldc * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+
+    CUtensorMap mb, ma0, ma1, mc;
+    if (!make_map_2d(&mb, weights, (uint64_t)L.kp, (uint64_t)L.np, (uint64_t)L.kp, PR_BK, (uint32_t)(prm.bn / 2),
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for B");
+    if (!make_map_2d(&ma0, a0, (uint64_t)a_pitch, (uint64_t)m, (uint64_t)a_pitch, 16, PR_BM,
+                     CU_TENSOR_MAP_SWIZZLE_NONE))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for A");
+    if (a_ternary) {
+        if (!make_map_2d(&ma1, a1, (uint64_t)a_pitch, (uint64_t)m, (uint64_t)a_pitch, 16, PR_BM,
+                         CU_TENSOR_MAP_SWIZZLE_NONE))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for A minus");
+    } else {
+        ma1 = ma0;
+    }
+    if (prm.tma_store) {
+        if (!make_map_2d(&mc, c, (uint64_t)n, (uint64_t)m, (uint64_t)ldc * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_DATA_TYPE_UINT16))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for C");
+    } else {
+        mc = ma0;
+    }
+
+    const int tiles = prm.m_tiles * prm.n_tiles;
+    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    if (a_ternary) {
+        static bool attr = false;
+        if (!attr) {
+            LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             PR_SMEM_BYTES));
+            attr = true;
+        }
+        gemm_tc_pair_kernel<true><<<2 * pairs, PR_THREADS, PR_SMEM_BYTES, stream>>>(mb, ma0, ma1, mc, prm);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_pair_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, PR_SMEM_BYTES));
+            attr = true;
+        }
+        gemm_tc_pair_kernel<false><<<2 * pairs, PR_THREADS, PR_SMEM_BYTES, stream>>>(mb, ma0, ma1, mc, prm);
+    }
+    LB_CUDA_TRY(cudaGetLastError());
+    return LOWBIT_OK;
+}
+
+}  // namespace lb

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 from oracle.oracle import BNN, TNN, TBN, a_mode_ternary, b_mode_ternary  # noqa: E402
 from tests.golden.make_golden import SMALL_GEMM, mode_dists, sweep_shapes  # noqa: E402
 
-KERNELS = [1, 2]  # LOWBIT_KERNEL_BITSERIAL, LOWBIT_KERNEL_TENSOR
+KERNELS = [1, 2, 3]  # LOWBIT_KERNEL_BITSERIAL, LOWBIT_KERNEL_TENSOR (pairs), LOWBIT_KERNEL_TENSOR_1CTA
 
 
 @pytest.fixture(scope="module")
@@ -255,7 +255,7 @@ def _row_col_sum_check(a, b, c):
     assert torch.equal(c_cols, want_cols)
 
 
-@pytest.mark.parametrize("kernel", [2])
+@pytest.mark.parametrize("kernel", [2, 3])
 def test_config3_full(lb, port, golden_configs, kernel):
     m = n = 8192
     k = 4096
