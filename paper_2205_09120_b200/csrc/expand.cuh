@@ -8,16 +8,10 @@ namespace lb {
 // k-block chunk (64 elements) -> int8 UMMA chunks 4h..4h+3 (16 B each) of the
 // K-major 128B-swizzled tile.  ~2 integer ops per element:
 //   nibble isolate (PRMT) -> spread4 (IMAD+LOP) -> minus*0xFF + plus (IMAD).
-template <bool A_TER>
-__device__ __forceinline__ void expand_half(uint32_t raw_p, uint32_t raw_m, uint32_t a_tile, int r, int h) {
-    const uint2 p = lds_v2(raw_p + r * 16 + 8 * h);
-    uint2 m = make_uint2(0, 0);
-    if (A_TER) m = lds_v2(raw_m + r * 16 + 8 * h);
-    const uint32_t row = a_tile + r * 128;
-    const int sw = r & 7;
-#pragma unroll
-    for (int wi = 0; wi < 2; ++wi) {
-        const uint32_t pw = wi ? p.y : p.x, mw = wi ? m.y : m.x;
+// 32 raw bits of each plane (one word) -> two 16-byte UMMA chunks (ch0, ch0+1).
+template <bool A_TER, int DBG = 0>
+__device__ __forceinline__ void expand_word(uint32_t pw, uint32_t mw, uint32_t row, int sw, int ch0) {
+    {
         const uint32_t p_lo = pw & 0x0F0F0F0Fu, p_hi = (pw >> 4) & 0x0F0F0F0Fu;
         const uint32_t m_lo = mw & 0x0F0F0F0Fu, m_hi = (mw >> 4) & 0x0F0F0F0Fu;
 #pragma unroll
@@ -38,10 +32,37 @@ __device__ __forceinline__ void expand_half(uint32_t raw_p, uint32_t raw_m, uint
                     w[2 * bb + 1] = (P1 * 0xFEu) ^ 0x01010101u;
                 }
             }
-            const int ch = 4 * h + 2 * wi + c;
-            sts_v4(row + ((ch ^ sw) << 4), w[0], w[1], w[2], w[3]);
+            const int ch = ch0 + c;
+            if (DBG == 2) {  // timing experiment: keep the ALU work, drop the stores
+                if ((w[0] ^ w[1] ^ w[2] ^ w[3]) == 0x9E3779B9u && pw == 0x7F4A7C15u) sts_v4(row, w[0], 0, 0, 0);
+            } else {
+                sts_v4(row + ((ch ^ sw) << 4), w[0], w[1], w[2], w[3]);
+            }
         }
     }
+}
+
+template <bool A_TER>
+__device__ __forceinline__ void expand_half(uint32_t raw_p, uint32_t raw_m, uint32_t a_tile, int r, int h) {
+    const uint2 p = lds_v2(raw_p + r * 16 + 8 * h);
+    uint2 m = make_uint2(0, 0);
+    if (A_TER) m = lds_v2(raw_m + r * 16 + 8 * h);
+    const uint32_t row = a_tile + r * 128;
+    expand_word<A_TER>(p.x, m.x, row, r & 7, 4 * h);
+    expand_word<A_TER>(p.y, m.y, row, r & 7, 4 * h + 2);
+}
+
+// Whole row: 16 raw bytes per plane -> the row's 8 chunks (128 int8).
+template <bool A_TER, int DBG = 0>
+__device__ __forceinline__ void expand_row(uint32_t raw_p, uint32_t raw_m, uint32_t a_tile, int r) {
+    const uint4 p = lds_v4(raw_p + r * 16);
+    uint4 m = make_uint4(0, 0, 0, 0);
+    if (A_TER) m = lds_v4(raw_m + r * 16);
+    const uint32_t row = a_tile + r * 128;
+    expand_word<A_TER, DBG>(p.x, m.x, row, r & 7, 0);
+    expand_word<A_TER, DBG>(p.y, m.y, row, r & 7, 2);
+    expand_word<A_TER, DBG>(p.z, m.z, row, r & 7, 4);
+    expand_word<A_TER, DBG>(p.w, m.w, row, r & 7, 6);
 }
 
 }  // namespace lb
