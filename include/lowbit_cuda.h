@@ -3,7 +3,7 @@
  * (paper_2205_09120_b200/liblowbit_cuda.so).
  *
  * This is the drop-in boundary for the reference library `lowbit`
- * (/root/reference/proj, namespace lowbit, headers include/lowbit/*.hpp).
+ * (/root/reference/proj, namespace lowbit, headers include/lowbit/<name>.hpp).
  * Every entry point names the reference interface it replaces.  Plain C:
  * pointers, sizes and status codes only; no C++ or torch types.  The C++
  * drop-in (paper_2205_09120_b200/cpp, namespace lowbit) and the Python
@@ -134,6 +134,44 @@ int lowbit_select_kernel(int mode, int m, int n, int k);
 lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t* a1, int a_rows, int a_cols,
                                       const uint8_t* panels, int b_ternary, int b_n, int b_k, int m, int n, int k,
                                       int k_blk, int16_t* c, int kernel, lowbit_stream stream);
+
+/* ---- K4: convolution (conv.hpp:64-65 conv2d_lowbit; conv.cpp:33-59) -------
+ * fm: NHWC int8 batch [batch][h][w][c] (the reference takes one image per
+ * call; batch > 1 is the same computation per image).  Output pixels
+ * (batch*OH*OW of them, lowbit_conv_rows) are the GeMM rows; depth
+ * k = kh*kw*c in (ky, kx, c) order (conv.cpp:18-27).
+ * lowbit_conv_encode: one launch of fused im2col + encode into the A planes
+ * (binary planes when a_binary, plus/minus otherwise; padded positions read
+ * as pad_value).  lowbit_conv2d: checks in the reference's order
+ * (ChannelOverflow, weight shape, modes, EmptyOutput), K4, then lowbit_gemm
+ * into out = int16 NHWC [batch][OH][OW][cout].  fm_binary is the feature
+ * map's Mode (binary maps pad with binary_pad_value, ternary maps with 0);
+ * a 0 in the A operand of a BNN conv sets *zero_flag. */
+long long lowbit_conv_rows(int batch, int h, int w, int kh, int kw, int stride, int padding);
+lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int batch, int h, int w, int c, int kh, int kw,
+                                 int stride, int padding, int pad_value, uint8_t* plane0, uint8_t* plane1,
+                                 long long pitch, int* zero_flag, lowbit_stream stream);
+size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int w, int c, int kh, int kw, int stride,
+                                     int padding);
+lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
+                            const void* weights, int b_ternary, int cout, int k, int kh, int kw, int stride,
+                            int padding, int binary_pad_value, void* workspace, int* zero_flag, int16_t* out,
+                            int kernel, lowbit_stream stream);
+/* Host-buffer drop-in of conv2d_lowbit: host NHWC fm, host PackedB panels of
+ * the (kh*kw*c) x cout weights, host int32 NHWC out (IntFeatureMap). */
+lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
+                                 const uint8_t* panels, int b_ternary, int cout, int k, int kh, int kw, int stride,
+                                 int padding, int binary_pad_value, int32_t* out, lowbit_stream stream);
+
+/* ---- host-buffer forms of K1 / K1b (used by the C++ drop-in) -------------
+ * Host planes use the reference stride ceil(cols/8) bytes.  Synchronous. */
+/* encode_binary / encode_ternary (core.hpp:63,66): returns
+ * LOWBIT_ZERO_IN_BINARY for a 0 in a binary matrix (core.cpp:23). */
+lowbit_status lowbit_encode_host(int ternary, const int8_t* values, int rows, int cols, uint8_t* plane0,
+                                 uint8_t* plane1, lowbit_stream stream);
+/* pack_b (gemm.hpp:75-76): host K x N planes -> host PackedB panel stream. */
+lowbit_status lowbit_pack_b_host(int ternary, const uint8_t* b0, const uint8_t* b1, int k, int n, uint8_t* panels,
+                                 lowbit_stream stream);
 
 /* ---- synthetic data (bench/tests): counter-based generator --------------
  * out[r][c] = f_dist(splitmix64(seed ^ matrix_id<<56 ^ ((row0+r)*cols + c)))

@@ -105,6 +105,13 @@ SIGNATURES = {
     "lowbit_gemm": (_I, [_I, _P, _P, _LL, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _LL, _I, _P]),
     "lowbit_select_kernel": (_I, [_I, _I, _I, _I]),
     "lowbit_gemm_lowbit_host": (_I, [_I, _P, _P, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P]),
+    "lowbit_conv_rows": (_LL, [_I, _I, _I, _I, _I, _I, _I]),
+    "lowbit_conv_encode": (_I, [_I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _LL, _P, _P]),
+    "lowbit_conv2d_workspace_bytes": (C.c_size_t, [_I, _I, _I, _I, _I, _I, _I, _I, _I]),
+    "lowbit_conv2d": (_I, [_I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
+    "lowbit_conv2d_host": (_I, [_I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
+    "lowbit_encode_host": (_I, [_I, _P, _I, _I, _P, _P, _P]),
+    "lowbit_pack_b_host": (_I, [_I, _P, _P, _I, _I, _P, _P]),
     "lowbit_generate": (_I, [_I, C.c_ulonglong, _I, _LL, _LL, _LL, _P, _P]),
 }
 

@@ -165,7 +165,7 @@ struct Scratch {
     }
 };
 struct HostCtx {
-    Scratch a0, a1, panels, weights, c;
+    Scratch a0, a1, panels, weights, c, vals, flag;
 };
 thread_local HostCtx g_ctx;
 }  // namespace
@@ -212,6 +212,60 @@ extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, co
                           kernel, stream)))
         return st;
     LB_CUDA_TRY(cudaMemcpyAsync(c, X.c.ptr, (size_t)m * n * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
+    LB_CUDA_TRY(cudaStreamSynchronize(s));
+    return LOWBIT_OK;
+}
+
+extern "C" lowbit_status lowbit_encode_host(int ternary, const int8_t* values, int rows, int cols, uint8_t* plane0,
+                                            uint8_t* plane1, lowbit_stream stream) {
+    if (rows < 0 || cols < 0) return set_error(LOWBIT_INVALID_ARGUMENT, "encode: negative shape");
+    if (rows == 0 || cols == 0) return LOWBIT_OK;
+    if (!values || !plane0 || (ternary && !plane1)) return set_error(LOWBIT_INVALID_ARGUMENT, "encode: NULL pointer");
+    lowbit_status st;
+    if ((st = lowbit_device_check())) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    HostCtx& X = g_ctx;
+    const long long sb = (cols + 7) / 8, pitch = lowbit_plane_pitch(cols);
+    const size_t vbytes = (size_t)rows * cols, pbytes = (size_t)rows * pitch;
+    LB_CUDA_TRY(X.vals.ensure(vbytes));
+    LB_CUDA_TRY(X.a0.ensure(pbytes));
+    if (ternary) LB_CUDA_TRY(X.a1.ensure(pbytes));
+    LB_CUDA_TRY(X.flag.ensure(sizeof(int)));
+    LB_CUDA_TRY(cudaMemsetAsync(X.flag.ptr, 0, sizeof(int), s));
+    LB_CUDA_TRY(cudaMemcpyAsync(X.vals.ptr, values, vbytes, cudaMemcpyHostToDevice, s));
+    if ((st = lowbit_encode(ternary, static_cast<const int8_t*>(X.vals.ptr), rows, cols, cols,
+                            static_cast<uint8_t*>(X.a0.ptr), ternary ? static_cast<uint8_t*>(X.a1.ptr) : nullptr,
+                            pitch, static_cast<int*>(X.flag.ptr), stream)))
+        return st;
+    int flag = 0;
+    LB_CUDA_TRY(cudaMemcpyAsync(&flag, X.flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LB_CUDA_TRY(cudaMemcpy2DAsync(plane0, sb, X.a0.ptr, pitch, sb, rows, cudaMemcpyDeviceToHost, s));
+    if (ternary) LB_CUDA_TRY(cudaMemcpy2DAsync(plane1, sb, X.a1.ptr, pitch, sb, rows, cudaMemcpyDeviceToHost, s));
+    LB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (!ternary && flag) return set_error(LOWBIT_ZERO_IN_BINARY, "binary matrix contains a zero element");
+    return LOWBIT_OK;
+}
+
+extern "C" lowbit_status lowbit_pack_b_host(int ternary, const uint8_t* b0, const uint8_t* b1, int k, int n,
+                                            uint8_t* panels, lowbit_stream stream) {
+    if (k <= 0 || n <= 0) return LOWBIT_OK;
+    if (!b0 || !panels || (ternary && !b1)) return set_error(LOWBIT_INVALID_ARGUMENT, "pack_b: NULL pointer");
+    lowbit_status st;
+    if ((st = lowbit_device_check())) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    HostCtx& X = g_ctx;
+    const size_t pbytes = (size_t)k * ((n + 7) / 8);
+    const size_t obytes = lowbit_packed_b_bytes(ternary, n, k);
+    LB_CUDA_TRY(X.a0.ensure(pbytes));
+    if (ternary) LB_CUDA_TRY(X.a1.ensure(pbytes));
+    LB_CUDA_TRY(X.panels.ensure(obytes));
+    LB_CUDA_TRY(cudaMemcpyAsync(X.a0.ptr, b0, pbytes, cudaMemcpyHostToDevice, s));
+    if (ternary) LB_CUDA_TRY(cudaMemcpyAsync(X.a1.ptr, b1, pbytes, cudaMemcpyHostToDevice, s));
+    if ((st = lowbit_pack_b(ternary, static_cast<const uint8_t*>(X.a0.ptr),
+                            ternary ? static_cast<const uint8_t*>(X.a1.ptr) : nullptr, k, n, (n + 7) / 8,
+                            static_cast<uint8_t*>(X.panels.ptr), stream)))
+        return st;
+    LB_CUDA_TRY(cudaMemcpyAsync(panels, X.panels.ptr, obytes, cudaMemcpyDeviceToHost, s));
     LB_CUDA_TRY(cudaStreamSynchronize(s));
     return LOWBIT_OK;
 }

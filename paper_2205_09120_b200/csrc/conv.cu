@@ -1,0 +1,225 @@
+// conv.cu — K4: convolution as fused im2col + encode, feeding the GeMM kernels.
+//
+// Reference: conv2d_lowbit = im2col -> encode_* -> pack_b -> gemm_lowbit ->
+// widen to int32 (conv.cpp:33-59), one image per call, (ky, kx, c) column
+// order, pad value 0 for ternary / binary_pad_value for binary activations.
+//
+// Here one launch reads the NHWC int8 batch and writes the implicit-GeMM A
+// operand directly as bit planes (the 9x-redundant int8 im2col matrix never
+// exists), then lowbit_gemm runs on it with M = batch*OH*OW.  Each thread
+// builds one 32-bit word (32 consecutive depth positions) of one output
+// pixel; when C % 32 == 0 a word is 32 contiguous channels of one input
+// pixel, read with two 16-byte loads (repeated taps hit L2).
+//
+// Algorithmic bytes per launch: batch*H*W*C int8 read + rows*pitch*planes written.
+#include <cstdio>
+
+#include "common.cuh"
+#include "encode.cuh"
+#include "layout.cuh"
+
+namespace lb {
+
+struct ConvGeom {
+    int batch, h, w, c, kh, kw, stride, pad, oh, ow, k;
+};
+
+// a_binary: write one binary plane (BNN's A) instead of plus/minus planes.
+__global__ void conv_encode_kernel(int a_binary, const int8_t* __restrict__ fm, ConvGeom g, int pad_value,
+                                   uint8_t* __restrict__ plane0, uint8_t* __restrict__ plane1, long long pitch,
+                                   int* zero_flag) {
+    const long long words_per_row = pitch / 4;
+    const long long rows = (long long)g.batch * g.oh * g.ow;
+    const long long total = rows * words_per_row;
+    const bool fast = (g.c % 32) == 0;
+    bool saw_zero = false;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long r = idx / words_per_row;
+        const int wd = (int)(idx - r * words_per_row);
+        const int img = (int)(r / (g.oh * g.ow));
+        const int rem = (int)(r - (long long)img * g.oh * g.ow);
+        const int oy = rem / g.ow, ox = rem - oy * g.ow;
+        const int k0 = wd * 32;
+        uint32_t plus = 0, minus = 0;
+        if (k0 < g.k) {
+            const int nvals = g.k - k0 < 32 ? g.k - k0 : 32;
+            if (fast) {
+                const int tap = k0 / g.c, c0 = k0 - tap * g.c;
+                const int ky = tap / g.kw, kx = tap - ky * g.kw;
+                const int y = oy * g.stride + ky - g.pad, x = ox * g.stride + kx - g.pad;
+                if (y >= 0 && y < g.h && x >= 0 && x < g.w) {
+                    encode_word32(fm + (((long long)img * g.h + y) * g.w + x) * g.c + c0, 32, plus, minus);
+                } else if (pad_value > 0) {
+                    plus = 0xFFFFFFFFu;
+                } else if (pad_value < 0) {
+                    minus = 0xFFFFFFFFu;
+                }
+            } else {
+                for (int j = 0; j < nvals; ++j) {
+                    const int kk = k0 + j;
+                    const int tap = kk / g.c, ch = kk - tap * g.c;
+                    const int ky = tap / g.kw, kx = tap - ky * g.kw;
+                    const int y = oy * g.stride + ky - g.pad, x = ox * g.stride + kx - g.pad;
+                    const int v = (y >= 0 && y < g.h && x >= 0 && x < g.w)
+                                      ? fm[(((long long)img * g.h + y) * g.w + x) * g.c + ch]
+                                      : pad_value;
+                    if (v > 0) plus |= 1u << j;
+                    if (v < 0) minus |= 1u << j;
+                }
+            }
+            if (a_binary && ((plus | minus) != valid_mask32(nvals))) saw_zero = true;
+        }
+        if (a_binary) {
+            reinterpret_cast<uint32_t*>(plane0 + r * pitch)[wd] = minus;
+        } else {
+            reinterpret_cast<uint32_t*>(plane0 + r * pitch)[wd] = plus;
+            reinterpret_cast<uint32_t*>(plane1 + r * pitch)[wd] = minus;
+        }
+    }
+    if (saw_zero && zero_flag) atomicOr(zero_flag, 1);
+}
+
+__global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+}  // namespace lb
+
+using namespace lb;
+
+static int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
+
+// conv.cpp:35-45 checks, in order, then the EmptyOutput of im2col (conv.cpp:12).
+static lowbit_status validate_conv(int mode, int batch, int h, int w, int c, int fm_binary, int b_ternary, int cout,
+                                   int k, int kh, int kw, int stride, int padding) {
+    const long long kk = (long long)kh * kw * c;
+    if (kk > LOWBIT_K_MAX16) {
+        char buf[128];
+        const long long cmax = LOWBIT_K_MAX16 / ((long long)kh * kw);
+        std::snprintf(buf, sizeof buf, "input channels %d exceed c_in_max %lld", c, cmax);
+        return lbhost::set_error(LOWBIT_CHANNEL_OVERFLOW, buf, c, cmax);
+    }
+    if (k != kk || cout < 1) return lbhost::set_error(LOWBIT_OUT_OF_BOUNDS, "out of bounds: weight matrix shape");
+    const bool a_binary = mode == LOWBIT_BNN, b_binary = mode != LOWBIT_TNN;
+    if (mode < 0 || mode > 2) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "unknown gemm mode");
+    if (a_binary && !fm_binary) return lbhost::set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: bnn requires binary activations");
+    if (b_binary && b_ternary) return lbhost::set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: weights must be binary");
+    if (!b_binary && !b_ternary) return lbhost::set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: weights must be ternary");
+    if (stride < 1 || batch < 1 || h < 0 || w < 0 || c < 1)
+        return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv: bad geometry");
+    if (conv_out(h, kh, stride, padding) < 1 || conv_out(w, kw, stride, padding) < 1)
+        return lbhost::set_error(LOWBIT_EMPTY_OUTPUT, "convolution produces empty output");
+    return LOWBIT_OK;
+}
+
+extern "C" long long lowbit_conv_rows(int batch, int h, int w, int kh, int kw, int stride, int padding) {
+    const int oh = conv_out(h, kh, stride, padding), ow = conv_out(w, kw, stride, padding);
+    if (oh < 1 || ow < 1 || batch < 1) return 0;
+    return (long long)batch * oh * ow;
+}
+
+extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int batch, int h, int w, int c, int kh,
+                                            int kw, int stride, int padding, int pad_value, uint8_t* plane0,
+                                            uint8_t* plane1, long long pitch, int* zero_flag, lowbit_stream stream) {
+    ConvGeom g{batch, h, w, c, kh, kw, stride, padding, conv_out(h, kh, stride, padding),
+               conv_out(w, kw, stride, padding), kh * kw * c};
+    if (g.oh < 1 || g.ow < 1) return lbhost::set_error(LOWBIT_EMPTY_OUTPUT, "convolution produces empty output");
+    if (!fm || !plane0 || (!a_binary && !plane1)) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv_encode: NULL");
+    if ((pitch & 3) || pitch < (g.k + 7) / 8)
+        return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv_encode: bad pitch");
+    const long long work = (long long)batch * g.oh * g.ow * (pitch / 4);
+    conv_encode_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(a_binary, fm, g, pad_value, plane0,
+                                                                               plane1, pitch, zero_flag);
+    LB_CUDA_TRY(cudaGetLastError());
+    return LOWBIT_OK;
+}
+
+extern "C" size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int w, int c, int kh, int kw, int stride,
+                                                int padding) {
+    const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
+    return (size_t)rows * lowbit_plane_pitch(kh * kw * c) * (mode == LOWBIT_BNN ? 1 : 2) + 256;
+}
+
+extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
+                                       const void* weights, int b_ternary, int cout, int k, int kh, int kw, int stride,
+                                       int padding, int binary_pad_value, void* workspace, int* zero_flag,
+                                       int16_t* out, int kernel, lowbit_stream stream) {
+    lowbit_status st = validate_conv(mode, batch, h, w, c, fm_binary, b_ternary, cout, k, kh, kw, stride, padding);
+    if (st) return st;
+    if (!workspace || !weights || !out) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d: NULL pointer");
+    const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
+    const long long pitch = lowbit_plane_pitch(k);
+    uint8_t* p0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    const int a_binary = mode == LOWBIT_BNN;
+    uint8_t* p1 = a_binary ? nullptr : p0 + rows * pitch;
+    // pad with 0 for ternary feature maps, binary_pad_value for binary ones (conv.cpp:13)
+    if ((st = lowbit_conv_encode(a_binary, fm, batch, h, w, c, kh, kw, stride, padding,
+                                 fm_binary ? binary_pad_value : 0, p0, p1, pitch, zero_flag, stream)))
+        return st;
+    if (rows > 0x7FFFFFFFLL) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d: too many output pixels");
+    return lowbit_gemm(mode, p0, p1, pitch, (int)rows, k, weights, b_ternary, cout, k, (int)rows, cout, k, 4096, out,
+                       cout, kernel, stream);
+}
+
+namespace {
+struct ConvScratch {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        want = (want + 0xFFFFF) & ~size_t(0xFFFFF);
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+};
+thread_local ConvScratch g_fm, g_ws, g_pan, g_w, g_out, g_out32, g_flag;
+}  // namespace
+
+extern "C" lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
+                                            const uint8_t* panels, int b_ternary, int cout, int k, int kh, int kw,
+                                            int stride, int padding, int binary_pad_value, int32_t* out,
+                                            lowbit_stream stream) {
+    lowbit_status st = validate_conv(mode, batch, h, w, c, fm_binary, b_ternary, cout, k, kh, kw, stride, padding);
+    if (st) return st;
+    if (!fm || !panels || !out) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d_host: NULL pointer");
+    if ((st = lowbit_device_check())) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
+    const size_t fm_bytes = (size_t)batch * h * w * c;
+    const size_t pbytes = lowbit_packed_b_bytes(b_ternary, cout, k);
+    LB_CUDA_TRY(g_fm.ensure(fm_bytes + 16));
+    LB_CUDA_TRY(g_ws.ensure(lowbit_conv2d_workspace_bytes(mode, batch, h, w, c, kh, kw, stride, padding)));
+    LB_CUDA_TRY(g_pan.ensure(pbytes));
+    LB_CUDA_TRY(g_w.ensure(lowbit_weights_bytes(b_ternary, cout, k)));
+    LB_CUDA_TRY(g_out.ensure((size_t)rows * cout * sizeof(int16_t)));
+    LB_CUDA_TRY(g_out32.ensure((size_t)rows * cout * sizeof(int32_t)));
+    LB_CUDA_TRY(g_flag.ensure(sizeof(int)));
+    LB_CUDA_TRY(cudaMemsetAsync(g_flag.ptr, 0, sizeof(int), s));
+    LB_CUDA_TRY(cudaMemcpyAsync(g_fm.ptr, fm, fm_bytes, cudaMemcpyHostToDevice, s));
+    LB_CUDA_TRY(cudaMemcpyAsync(g_pan.ptr, panels, pbytes, cudaMemcpyHostToDevice, s));
+    if ((st = lowbit_prepare_weights(b_ternary, static_cast<const uint8_t*>(g_pan.ptr), cout, k, g_w.ptr, stream)))
+        return st;
+    if ((st = lowbit_conv2d(mode, static_cast<const int8_t*>(g_fm.ptr), batch, h, w, c, fm_binary, g_w.ptr, b_ternary,
+                            cout, k, kh, kw, stride, padding, binary_pad_value, g_ws.ptr,
+                            static_cast<int*>(g_flag.ptr), static_cast<int16_t*>(g_out.ptr), LOWBIT_KERNEL_AUTO,
+                            stream)))
+        return st;
+    const long long n = rows * cout;
+    widen_kernel<<<grid_for(n, 256), 256, 0, s>>>(static_cast<const int16_t*>(g_out.ptr),
+                                                    static_cast<int32_t*>(g_out32.ptr), n);
+    LB_CUDA_TRY(cudaGetLastError());
+    int flag = 0;
+    LB_CUDA_TRY(cudaMemcpyAsync(&flag, g_flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LB_CUDA_TRY(cudaMemcpyAsync(out, g_out32.ptr, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    LB_CUDA_TRY(cudaStreamSynchronize(s));
+    // a 0 among binary activations (or a 0 binary pad value) is what
+    // encode_binary(cols) rejects in the reference (conv.cpp:51, core.cpp:23)
+    if (mode == LOWBIT_BNN && flag) return lbhost::set_error(LOWBIT_ZERO_IN_BINARY, "binary matrix contains a zero element");
+    return LOWBIT_OK;
+}

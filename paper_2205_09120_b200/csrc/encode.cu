@@ -8,12 +8,12 @@
 // Algorithmic bytes (roofline denominators):
 //   encode: rows*cols int8 read + planes*rows*pitch written.
 #include "common.cuh"
+#include "encode.cuh"
 #include "layout.cuh"
 
 namespace lb {
 
 // One thread -> one 32-bit word of every plane of one row (32 values).
-// Vector path: 2 x 16-byte loads when the row chunk is aligned and complete.
 __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, int rows, int cols, long long ld,
                               uint8_t* __restrict__ plane0, uint8_t* __restrict__ plane1, long long pitch,
                               int* zero_flag) {
@@ -27,29 +27,9 @@ __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, in
         const int c0 = w * 32;
         uint32_t minus = 0, plus = 0;
         if (c0 < cols) {
-            const int8_t* src = values + r * ld + c0;
             const int nvals = cols - c0 < 32 ? cols - c0 : 32;
-            if (nvals == 32 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-                const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
-                const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-                const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const uint32_t neg = gather_msb4(v[q]);
-                    const uint32_t nz = gather_msb4(nonzero_msb(v[q]));
-                    minus |= neg << (4 * q);
-                    plus |= (nz & ~neg) << (4 * q);
-                }
-            } else {
-                for (int j = 0; j < nvals; ++j) {
-                    const int8_t x = src[j];
-                    if (x < 0) minus |= 1u << j;
-                    if (x > 0) plus |= 1u << j;
-                }
-            }
-            // A zero among the valid lanes: plus|minus misses a valid bit.
-            const uint32_t valid = nvals == 32 ? 0xFFFFFFFFu : ((1u << nvals) - 1u);
-            if (!ternary && ((plus | minus) != valid)) saw_zero = true;
+            encode_word32(values + r * ld + c0, nvals, plus, minus);
+            if (!ternary && ((plus | minus) != valid_mask32(nvals))) saw_zero = true;
         }
         uint32_t* d0 = reinterpret_cast<uint32_t*>(plane0 + r * pitch);
         if (ternary) {
@@ -217,13 +197,6 @@ __global__ void generate_kernel(int dist, uint64_t seed, int matrix_id, long lon
         }
         out[i] = v;
     }
-}
-
-static int grid_for(long long work, int threads) {
-    long long g = (work + threads - 1) / threads;
-    const long long cap = 148LL * 16;  // 16 resident 256-thread blocks per SM
-    if (g > cap) g = cap;
-    return (int)(g < 1 ? 1 : g);
 }
 
 }  // namespace lb
