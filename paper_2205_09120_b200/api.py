@@ -177,3 +177,34 @@ def generate(dist: int, seed: int, matrix_id: int, rows: int, cols: int, row0: i
 
 def select_kernel(mode: int, m: int, n: int, k: int) -> int:
     return int(L.lib.lowbit_select_kernel(mode, m, n, k))
+
+
+def conv_out_dim(i: int, k: int, s: int, p: int) -> int:
+    """conv.cpp:5-7"""
+    return (i + 2 * p - k) // s + 1
+
+
+def conv2d_lowbit(mode: int, fm: torch.Tensor, fm_binary: bool, weights: Weights, kh: int, kw: int, stride: int = 1,
+                  padding: int = 0, binary_pad_value: int = 1, kernel: int = KERNEL_AUTO,
+                  out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """conv2d_lowbit (conv.cpp:33-59) over an NHWC int8 batch [B, H, W, C]:
+    K4 fused im2col+encode, then the GeMM kernels.  weights: the prepared
+    (kh*kw*C) x cout sign matrix.  Returns int16 [B, OH, OW, cout]."""
+    if fm.dim() == 3:
+        fm = fm.unsqueeze(0)
+    fm = fm.contiguous()
+    b, h, w, c = fm.shape
+    oh, ow = conv_out_dim(h, kh, stride, padding), conv_out_dim(w, kw, stride, padding)
+    cout = weights.n
+    if out is None:
+        out = torch.empty((b, max(oh, 1), max(ow, 1), cout), dtype=torch.int16, device=fm.device)
+    if workspace is None:
+        nbytes = int(L.lib.lowbit_conv2d_workspace_bytes(mode, b, h, w, c, kh, kw, stride, padding))
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=fm.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=fm.device)
+    L.check(L.lib.lowbit_conv2d(mode, _ptr(fm), b, h, w, c, int(fm_binary), _ptr(weights.buf), int(weights.ternary),
+                                cout, weights.k, kh, kw, stride, padding, binary_pad_value, _ptr(workspace),
+                                _ptr(flag), _ptr(out), kernel, _stream()), "conv2d_lowbit")
+    if mode == BNN and int(flag.item()):
+        raise L.ZeroInBinaryInput("binary matrix contains a zero element")
+    return out

@@ -1,0 +1,96 @@
+"""GPU parity for K4 (fused im2col + encode) + GeMM = conv2d_lowbit
+(conv.cpp:33-59), against the oracle's 6-loop direct convolution
+(test_conv.cpp:22-47 restated in oracle/lowbit_oracle.c) and the reference's
+own output hash for BASELINE.json config 4."""
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import BNN, TNN, TBN  # noqa: E402
+from tests.golden.make_golden import mode_dists  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2205_09120_b200 as lb
+    return lb
+
+
+def weights_for(lb, wt, mode):
+    t = torch.from_numpy(np.ascontiguousarray(wt)).cuda()
+    bp = lb.encode_ternary(t) if mode == TNN else lb.encode_binary(t)
+    return lb.prepare_weights(lb.pack_b(bp))
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_conv_shape_suite(lb, port, mode, kernel):  # test_conv.cpp:118-138
+    da, db = mode_dists(mode)
+    i = 0
+    for spatial in (1, 3, 5, 8, 9):
+        for ch in (1, 5, 32, 64):
+            for ksz in (1, 3):
+                for stride in (1, 2):
+                    for pad in (0, 1):
+                        if spatial + 2 * pad < ksz:
+                            continue
+                        i += 1
+                        batch = 2
+                        fm = port.generate(da, 56, 3 * i, batch * spatial * spatial, ch).reshape(batch, spatial,
+                                                                                                 spatial, ch)
+                        wt = port.generate(db, 56, 3 * i + 1, ksz * ksz * ch, 4)
+                        w = weights_for(lb, wt, mode)
+                        got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), mode == BNN, w, ksz, ksz, stride,
+                                               pad, kernel=kernel).cpu().numpy()
+                        for img in range(batch):
+                            want = port.direct_conv(fm[img], mode == BNN, wt, ksz, ksz, stride, pad)
+                            assert (got[img].astype(np.int32) == want).all(), (mode, spatial, ch, ksz, stride, pad)
+
+
+def test_conv_binary_pad_values(lb, port):  # test_conv.cpp:140-149
+    fm = port.generate(1, 57, 0, 9, 2).reshape(3, 3, 2)
+    wt = port.generate(1, 57, 1, 18, 2)
+    w = weights_for(lb, wt, BNN)
+    for pv in (1, -1):
+        got = lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, w, 3, 3, 1, 1, binary_pad_value=pv)
+        assert (got[0].cpu().numpy().astype(np.int32) == port.direct_conv(fm, True, wt, 3, 3, 1, 1, pv)).all()
+    with pytest.raises(lb.ZeroInBinaryInput):  # a 0 pad is a 0 in encode_binary(cols)
+        lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, w, 3, 3, 1, 1, binary_pad_value=0)
+    # TBN pads a binary map with the pad value too, but encodes it ternary: 0 is allowed
+    wtb = port.generate(1, 57, 2, 18, 2)
+    got = lb.conv2d_lowbit(TBN, torch.from_numpy(fm).cuda(), True, weights_for(lb, wtb, TBN), 3, 3, 1, 1,
+                           binary_pad_value=0)
+    assert (got[0].cpu().numpy().astype(np.int32) == port.direct_conv(fm, True, wtb, 3, 3, 1, 1, 0)).all()
+
+
+def test_conv_errors(lb, port):  # test_conv.cpp:151-164, conv.cpp:35-45
+    w = weights_for(lb, np.zeros((9 * 3641, 1), np.int8), TNN)
+    with pytest.raises(lb.ChannelOverflow) as e:
+        lb.conv2d_lowbit(TNN, torch.zeros((1, 1, 3641), dtype=torch.int8, device="cuda"), False, w, 3, 3, 1, 1)
+    assert (e.value.c_in, e.value.c_in_max) == (3641, 3640)
+    w_ok = weights_for(lb, np.zeros((9 * 3640, 1), np.int8), TNN)
+    out = lb.conv2d_lowbit(TNN, torch.zeros((3, 3, 3640), dtype=torch.int8, device="cuda"), False, w_ok, 3, 3, 1, 0)
+    assert out.shape[1:3] == (1, 1) and int(out[0, 0, 0, 0]) == 0
+    with pytest.raises(lb.EmptyOutput):
+        lb.conv2d_lowbit(TNN, torch.zeros((2, 2, 1), dtype=torch.int8, device="cuda"), False,
+                         weights_for(lb, np.zeros((9, 1), np.int8), TNN), 3, 3, 1, 0)
+    with pytest.raises(lb.ModeMismatch):
+        lb.conv2d_lowbit(BNN, torch.ones((3, 3, 1), dtype=torch.int8, device="cuda"), False,
+                         weights_for(lb, np.ones((9, 1), np.int8), BNN), 3, 3, 1, 0)
+
+
+def test_config4_full(lb, golden_configs):
+    # 64 x 56 x 56 x 128 NHWC ternary, 3x3x128 -> 128, stride 1, pad 1 (M=200704, K=1152, N=128)
+    fm = lb.generate(0, 46, 0, 64 * 56 * 56, 128).view(64, 56, 56, 128)
+    wt = lb.generate(0, 46, 1, 9 * 128, 128)
+    w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(wt)))
+    for kernel in (2, 1):
+        out = lb.conv2d_lowbit(TNN, fm, False, w, 3, 3, 1, 1, kernel=kernel)
+        h = hashlib.sha256(out.cpu().numpy().astype("<i2").tobytes()).hexdigest()
+        assert h == golden_configs["c4"]["sha256"], kernel
