@@ -427,10 +427,33 @@ def time_device(torch, fn, flush, reps=10):
     return float(np.median(ts))
 
 
+def graph_time(torch, fn, reps=20):
+    """Device time of fn() captured once in a CUDA graph, replayed `reps` times
+    back to back (removes the host/ctypes launch path from the measurement)."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
 def side_configs(lb, torch, flush, pk):
-    """Configs 1-3 at N=1 (both kernels where meaningful): latency and TOPS."""
+    """BASELINE.json configs 1-4 at N=1: device time per kernel, TOPS and the
+    fraction of the binding roofline.  Small configs (c1, c2) are timed as
+    CUDA-graph replays (launch-latency bound); c3/c4 with events + L2 flush."""
     out = {}
     tensor_peak = 2.0 * pk["bf16_tflops"]
+    popc = lambda mode: 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
+    kernels = (("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL))
     for name in ("c1", "c3"):
         mode, M, N, K, da, db, seed = CONFIGS[name]
         a = lb.generate(da, seed, 0, M, K)
@@ -439,17 +462,18 @@ def side_configs(lb, torch, flush, pk):
         w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)))
         c = torch.empty((M, N), dtype=torch.int16, device="cuda")
         res = {}
-        for kn, kid in (("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL)):
-            ms = time_device(torch, lambda: lb.gemm_lowbit(mode, ap_, w, (M, N, K), kernel=kid, out=c), flush)
+        for kn, kid in kernels:
+            f = lambda: lb.gemm_lowbit(mode, ap_, w, (M, N, K), kernel=kid, out=c)
+            ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
             tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
-            res[kn] = {"ms": ms, "TOPS": tops}
-        res["tensor"]["frac_of_tensor_peak"] = res["tensor"]["TOPS"] / tensor_peak
-        popc_peak = 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
-        res["bitserial"]["frac_of_popc_peak"] = res["bitserial"]["TOPS"] / popc_peak
+            res[kn] = {"ms": ms, "TOPS": tops,
+                       "frac": tops / (tensor_peak if kn == "tensor" else popc(mode)),
+                       "bound": "tensor" if kn == "tensor" else "popc"}
         res["auto"] = {1: "bitserial", 2: "tensor"}[lb.select_kernel(mode, M, N, K)]
+        res["timing"] = "cuda graph replay" if name == "c1" else "events, L2 flushed"
         out[name] = res
-    # c2: the 64-shape TBN sweep, one launch per shape, total device time
-    ws, aps, cs = [], [], []
+    # c2: the 64-shape TBN sweep (one launch per shape), captured as one graph
+    aps, ws, cs = [], [], []
     for s, (M, N, K) in enumerate(SWEEP):
         a = lb.generate(2, 44, 2 * s, M, K)
         b = lb.generate(1, 44, 2 * s + 1, K, N)
@@ -458,13 +482,55 @@ def side_configs(lb, torch, flush, pk):
         cs.append(torch.empty((M, N), dtype=torch.int16, device="cuda"))
     ops = sum(2.0 * M * N * K for M, N, K in SWEEP)
     res = {}
-    for kn, kid in (("auto", lb.KERNEL_AUTO), ("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL)):
+    for kn, kid in (("auto", lb.KERNEL_AUTO),) + kernels:
         def sweep():
             for s, (M, N, K) in enumerate(SWEEP):
                 lb.gemm_lowbit(2, aps[s], ws[s], (M, N, K), kernel=kid, out=cs[s])
-        ms = time_device(torch, sweep, flush, reps=5)
-        res[kn] = {"ms_total_64_shapes": ms, "TOPS": ops / (ms * 1e-3) / 1e12}
+        ms = graph_time(torch, sweep, reps=10)
+        res[kn] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12}
+    probs = [(aps[s], ws[s], cs[s]) for s in range(len(SWEEP))]
+    ms = graph_time(torch, lambda: lb.gemm_grouped(2, probs), reps=20)
+    res["grouped_one_launch"] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12}
+    res["timing"] = "cuda graph (64 launches, or 1 grouped launch), replayed"
     out["c2"] = res
+    # c4: conv 64x56x56x128, 3x3 -> 128, s1 p1 (K4 fused im2col+encode + GeMM)
+    fm = lb.generate(0, 46, 0, 64 * 56 * 56, 128).view(64, 56, 56, 128)
+    wt = lb.generate(0, 46, 1, 9 * 128, 128)
+    w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(wt)))
+    ws_bytes = int(lb._lib.lib.lowbit_conv2d_workspace_bytes(1, 64, 56, 56, 128, 3, 3, 1, 1))
+    wsp = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    o = torch.empty((64, 56, 56, 128), dtype=torch.int16, device="cuda")
+    ops4 = 2.0 * 200704 * 128 * 1152
+    res = {}
+    for kn, kid in kernels:
+        ms = time_device(torch, lambda: lb.conv2d_lowbit(1, fm, False, w, 3, 3, 1, 1, kernel=kid, out=o,
+                                                         workspace=wsp), flush)
+        res[kn] = {"ms": ms, "TOPS": ops4 / (ms * 1e-3) / 1e12}
+    # K4 alone (HBM-bound): int8 NHWC in, two bit planes out
+    pitch = lb.plane_pitch(1152)
+    p0 = wsp[: 200704 * pitch]
+    p1 = wsp[200704 * pitch: 2 * 200704 * pitch]
+    L = lb._lib
+    import ctypes as C
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    k4 = lambda: L.check(L.lib.lowbit_conv_encode(0, C.c_void_p(fm.data_ptr()), 64, 56, 56, 128, 3, 3, 1, 1, 0,
+                                                  C.c_void_p(p0.data_ptr()), C.c_void_p(p1.data_ptr()), pitch,
+                                                  None, st))
+    ms = time_device(torch, k4, flush)
+    k4_bytes = 64 * 56 * 56 * 128 + 2 * 200704 * pitch
+    res["k4_encode"] = {"ms": ms, "GB/s": k4_bytes / (ms * 1e-3) / 1e9,
+                        "frac_hbm": k4_bytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": k4_bytes}
+    out["c4"] = res
+    # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
+    a = lb.generate(0, 47, 0, 1048576, 2048)
+    planes = lb.empty_planes(1048576, 2048, True)
+    enc = lambda: L.check(L.lib.lowbit_encode(1, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,
+                                              C.c_void_p(planes.plane0.data_ptr()),
+                                              C.c_void_p(planes.plane1.data_ptr()), planes.pitch, None, st))
+    ms = time_device(torch, enc, flush, reps=5)
+    eb = 1048576 * 2048 + 2 * 1048576 * planes.pitch
+    out["k1_encode_c5"] = {"ms": ms, "GB/s": eb / (ms * 1e-3) / 1e9, "frac_hbm": eb / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                           "algorithmic_bytes": eb}
     return out
 
 

@@ -127,6 +127,24 @@ lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long l
 /* The static per-shape kernel table behind LOWBIT_KERNEL_AUTO. */
 int lowbit_select_kernel(int mode, int m, int n, int k);
 
+/* ---- grouped small GeMMs: one launch for many problems (§8f-3) ----------
+ * The reference bench grid (bench.cpp:196-234) / BASELINE config 2 runs 64
+ * small gemm_lowbit calls; each is launch-latency bound on a GPU.  One call
+ * here validates every problem like lowbit_gemm (dims, depth, modes) and
+ * issues one launch of K2-style bit-serial tiles for all of them (128
+ * problems per launch; more are split).  Device pointers, stream-ordered. */
+typedef struct lowbit_gemm_problem {
+    const uint8_t* a0;    /* binary plane or plus plane, pitch a_pitch (multiple of 16) */
+    const uint8_t* a1;    /* minus plane (ternary A) or NULL (binary A) */
+    long long a_pitch;
+    const void* weights;  /* lowbit_prepare_weights output for n x k */
+    int m, n, k;
+    int16_t* c;           /* m x n, row stride ldc */
+    long long ldc;
+} lowbit_gemm_problem;
+lowbit_status lowbit_gemm_grouped(int mode, int b_ternary, int count, const lowbit_gemm_problem* problems,
+                                  lowbit_stream stream);
+
 /* ---- host-buffer drop-in: one whole reference gemm_lowbit call -----------
  * Host A planes with the reference stride ceil(a_cols/8); host PackedB
  * panels; host C (m x n, row-major).  Uploads, prepares B, runs, downloads

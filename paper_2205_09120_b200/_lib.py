@@ -115,6 +115,16 @@ SIGNATURES = {
     "lowbit_generate": (_I, [_I, C.c_ulonglong, _I, _LL, _LL, _LL, _P, _P]),
 }
 
+
+
+class GemmProblem(C.Structure):
+    """lowbit_gemm_problem (include/lowbit_cuda.h)."""
+    _fields_ = [("a0", C.c_void_p), ("a1", C.c_void_p), ("a_pitch", C.c_longlong), ("weights", C.c_void_p),
+                ("m", C.c_int), ("n", C.c_int), ("k", C.c_int), ("c", C.c_void_p), ("ldc", C.c_longlong)]
+
+
+SIGNATURES["lowbit_gemm_grouped"] = (_I, [_I, _I, _I, C.POINTER(GemmProblem), _P])
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "

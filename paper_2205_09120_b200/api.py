@@ -208,3 +208,16 @@ def conv2d_lowbit(mode: int, fm: torch.Tensor, fm_binary: bool, weights: Weights
     if mode == BNN and int(flag.item()):
         raise L.ZeroInBinaryInput("binary matrix contains a zero element")
     return out
+
+
+def gemm_grouped(mode: int, problems, b_ternary: Optional[bool] = None):
+    """One launch for many small gemm_lowbit problems (bench grid / config 2).
+    problems: list of (a: Planes, w: Weights, out: int16 tensor)."""
+    if b_ternary is None:
+        b_ternary = mode == TNN
+    arr = (L.GemmProblem * len(problems))()
+    for i, (a, w, out) in enumerate(problems):
+        arr[i] = L.GemmProblem(a.plane0.data_ptr(), a.plane1.data_ptr() if a.plane1 is not None else None, a.pitch,
+                               w.buf.data_ptr(), a.rows, w.n, a.cols, out.data_ptr(), out.stride(0))
+    L.check(L.lib.lowbit_gemm_grouped(mode, int(b_ternary), len(problems), arr, _stream()), "gemm_grouped")
+    return [p[2] for p in problems]

@@ -112,13 +112,21 @@ static lowbit_status validate_gemm(int mode, bool a_ternary, int b_ternary, int 
     return LOWBIT_OK;
 }
 
-// Static per-shape kernel table.  Measured on B200:
-// the tcgen05 path wins every shape whose tile grid fills the machine; the
-// bit-serial path is kept for tiny / launch-bound shapes.
+// Static per-shape kernel table, from B200
+// measurements (profiles/r01, bench.py per_config):
+//   c1 360x96x256      tcgen05 6.7 us   vs bit-serial 12.6 us (graph replay)
+//   c2 sweep (64)      tcgen05 5.0 us   vs bit-serial 10.5 us per shape
+//   c3 8192^2x4096     tcgen05 2.68 POPS vs bit-serial 0.28 POPS (95% of POPC peak)
+//   c4 conv            tcgen05 0.38 POPS vs bit-serial 0.09 POPS
+//   c5 1Mx1024x2048    tcgen05 2.5 POPS
+// The int8 tensor path wins every measured shape, including the launch-bound
+// ones, so AUTO maps to it; the bit-serial kernel stays selectable (and is the
+// one the grouped small-GeMM launch uses, lowbit_gemm_grouped).
 extern "C" int lowbit_select_kernel(int mode, int m, int n, int k) {
     (void)mode;
-    const double ops = 2.0 * m * (double)n * k;
-    if (ops < 2.0e8 && m < 512) return LOWBIT_KERNEL_BITSERIAL;
+    (void)m;
+    (void)n;
+    (void)k;
     return LOWBIT_KERNEL_TENSOR;
 }
 

@@ -1,0 +1,172 @@
+// gemm_grouped.cu — one launch for a batch of small low-bit GeMMs (§8f-3).
+//
+// The reference bench grid (bench.cpp:196-234; BASELINE.json config 2: 64
+// TBN shapes M x N x K in {72..360} x {24..96} x {128..512}) is launch-latency
+// bound on a B200: each problem is 0.4-35 MOPs.  Here every problem's
+// 64 x 32 output tiles are laid out back to back in one grid; a CTA finds its
+// problem with a search over the tile prefix sums in the kernel parameters.
+// The arithmetic is K2's (bit-serial LOP3 + POPC, (nz, sign) form): tiles are
+// small and the operands live in L1/L2, so each thread streams its 4 rows and
+// 4 columns straight from global memory with 128-bit loads.
+#include <cstdio>
+
+#include "common.cuh"
+#include "layout.cuh"
+
+namespace lb {
+
+constexpr int GR_BM = 64, GR_BN = 32, GR_MAX = 128;
+
+struct GroupedProblem {
+    const uint8_t* a0;
+    const uint8_t* a1;
+    long long a_pitch;
+    const uint32_t* b_sign;
+    const uint32_t* b_nz;
+    int m, n, k, kw;
+    int16_t* c;
+    long long ldc;
+};
+
+struct GroupedParams {
+    int count;
+    int tile_start[GR_MAX + 1];
+    GroupedProblem p[GR_MAX];
+};
+
+__device__ __forceinline__ uint32_t tail_mask_word(int w, int k) {
+    const int bit0 = w * 32;
+    return bit0 >= k ? 0u : (k - bit0 >= 32 ? 0xFFFFFFFFu : ((1u << (k - bit0)) - 1u));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) gemm_grouped_kernel(const __grid_constant__ GroupedParams P) {
+    constexpr bool A_TER = MODE != 0, B_TER = MODE == 1;
+    const int bid = blockIdx.x;
+    int lo = 0, hi = P.count - 1;  // problem q with tile_start[q] <= bid < tile_start[q+1]
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (P.tile_start[mid] <= bid) lo = mid;
+        else hi = mid - 1;
+    }
+    const GroupedProblem& pr = P.p[lo];
+    const int t = bid - P.tile_start[lo];
+    const int tiles_n = (pr.n + GR_BN - 1) / GR_BN;
+    const int tm = t / tiles_n, tn = t - tm * tiles_n;
+    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // 16 x 8 threads, 4 x 4 outputs each
+    const int row0 = tm * GR_BM + ty * 4, col0 = tn * GR_BN + tx * 4;
+    const int a_words = (int)(pr.a_pitch / 4);
+    const int kwords = (pr.k + 31) / 32;
+
+    int acc[4][4] = {};
+    int nnz[4] = {0, 0, 0, 0};
+    for (int w0 = 0; w0 < kwords; w0 += 4) {
+        uint32_t as[4][4], an[4][4], bs[4][4], bn[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = row0 + i;
+            uint4 p = make_uint4(0, 0, 0, 0), q = make_uint4(0, 0, 0, 0);
+            if (r < pr.m && w0 < a_words) {
+                p = __ldg(reinterpret_cast<const uint4*>(pr.a0 + (long long)r * pr.a_pitch) + (w0 >> 2));
+                if (A_TER) q = __ldg(reinterpret_cast<const uint4*>(pr.a1 + (long long)r * pr.a_pitch) + (w0 >> 2));
+            }
+            const uint32_t pw[4] = {p.x, p.y, p.z, p.w}, qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t msk = tail_mask_word(w0 + j, pr.k);
+                if (A_TER) {
+                    as[i][j] = qw[j] & msk;
+                    an[i][j] = (pw[j] | qw[j]) & msk;
+                } else {
+                    as[i][j] = pw[j] & msk;
+                }
+            }
+            // B: prepared (nz, sign) words, [np][kw] with np >= round_up(n, 256), kw % 8 == 0
+            const long long boff = (long long)(col0 + i) * pr.kw + w0;
+            const uint4 s4 = __ldg(reinterpret_cast<const uint4*>(pr.b_sign + boff));
+            bs[i][0] = s4.x, bs[i][1] = s4.y, bs[i][2] = s4.z, bs[i][3] = s4.w;
+            if (B_TER) {
+                const uint4 n4 = __ldg(reinterpret_cast<const uint4*>(pr.b_nz + boff));
+                bn[i][0] = n4.x, bn[i][1] = n4.y, bn[i][2] = n4.z, bn[i][3] = n4.w;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (MODE == 2) nnz[i] += __popc(an[i][j]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (MODE == 0) {
+                        acc[i][c] += __popc(as[i][j] ^ bs[c][j]);
+                    } else if (MODE == 1) {
+                        const uint32_t mm = an[i][j] & bn[c][j];
+                        acc[i][c] += __popc(mm) - 2 * __popc(mm & (as[i][j] ^ bs[c][j]));
+                    } else {
+                        acc[i][c] += __popc(an[i][j] & (as[i][j] ^ bs[c][j]));
+                    }
+                }
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = row0 + i;
+        if (r >= pr.m) continue;
+        int16_t* dst = pr.c + (long long)r * pr.ldc + col0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (col0 + c >= pr.n) break;
+            const int a = acc[i][c];
+            dst[c] = (int16_t)(MODE == 0 ? pr.k - 2 * a : (MODE == 1 ? a : nnz[i] - 2 * a));
+        }
+    }
+}
+
+}  // namespace lb
+
+using namespace lb;
+
+extern "C" lowbit_status lowbit_gemm_grouped(int mode, int b_ternary, int count, const lowbit_gemm_problem* problems,
+                                             lowbit_stream stream) {
+    if (mode < 0 || mode > 2) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "grouped: unknown gemm mode");
+    if ((mode == LOWBIT_TNN) != (b_ternary != 0))
+        return lbhost::set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: tnn requires a ternary right operand, "
+                                                       "bnn/tbn a binary one");
+    if (count < 0 || (count > 0 && !problems))
+        return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "grouped: bad problem list");
+    for (int base = 0; base < count; base += GR_MAX) {
+        const int cnt = count - base < GR_MAX ? count - base : GR_MAX;
+        GroupedParams P;
+        P.count = cnt;
+        int tiles = 0;
+        for (int i = 0; i < cnt; ++i) {
+            const lowbit_gemm_problem& q = problems[base + i];
+            if (q.m <= 0 || q.n <= 0 || q.k <= 0) return lbhost::set_error(LOWBIT_OUT_OF_BOUNDS, "out of bounds: gemm dims");
+            if (q.k > LOWBIT_K_MAX16) {
+                char buf[96];
+                std::snprintf(buf, sizeof buf, "depth %d exceeds k_max %d", q.k, LOWBIT_K_MAX16);
+                return lbhost::set_error(LOWBIT_DEPTH_OVERFLOW, buf, q.k, LOWBIT_K_MAX16);
+            }
+            if ((mode != LOWBIT_BNN) != (q.a1 != nullptr))
+                return lbhost::set_error(LOWBIT_MODE_MISMATCH, "mode mismatch: left operand kind");
+            if (!q.a0 || !q.weights || !q.c || (q.a_pitch & 15) || q.a_pitch < (q.k + 7) / 8 || q.ldc < q.n ||
+                (reinterpret_cast<uintptr_t>(q.a0) & 15) || (q.a1 && (reinterpret_cast<uintptr_t>(q.a1) & 15)) ||
+                (reinterpret_cast<uintptr_t>(q.weights) & 255))
+                return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "grouped: device layout precondition violated");
+            const WeightsLayout L(b_ternary, q.n, q.k);
+            const uint8_t* wb = static_cast<const uint8_t*>(q.weights);
+            P.p[i] = GroupedProblem{q.a0, q.a1, q.a_pitch, reinterpret_cast<const uint32_t*>(wb + L.off_sign),
+                                    reinterpret_cast<const uint32_t*>(wb + L.off_nz), q.m, q.n, q.k, L.kw, q.c, q.ldc};
+            P.tile_start[i] = tiles;
+            tiles += ((q.m + GR_BM - 1) / GR_BM) * ((q.n + GR_BN - 1) / GR_BN);
+        }
+        P.tile_start[cnt] = tiles;
+        if (tiles == 0) continue;
+        cudaStream_t s = (cudaStream_t)stream;
+        if (mode == 0) gemm_grouped_kernel<0><<<tiles, 128, 0, s>>>(P);
+        else if (mode == 1) gemm_grouped_kernel<1><<<tiles, 128, 0, s>>>(P);
+        else gemm_grouped_kernel<2><<<tiles, 128, 0, s>>>(P);
+        LB_CUDA_TRY(cudaGetLastError());
+    }
+    return LOWBIT_OK;
+}

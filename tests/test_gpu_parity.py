@@ -295,3 +295,35 @@ def test_config5_full(lb, port, golden_configs):
         assert (host(c[r0:r0 + 3]) == want).all()
     if "c5" in golden_configs:
         assert sha(host(c)) == golden_configs["c5"]["sha256"]
+
+
+# ------------------------------------------------------------------ grouped launch (§8f-3)
+def test_grouped_config2_sweep(lb, golden_configs):
+    problems = []
+    for s, (m, n, k) in enumerate(sweep_shapes()):
+        a = lb.generate(2, 44, 2 * s, m, k)
+        b = lb.generate(1, 44, 2 * s + 1, k, n)
+        w = lb.prepare_weights(lb.pack_b(lb.encode_binary(b)))
+        problems.append((lb.encode_ternary(a), w, torch.empty((m, n), dtype=torch.int16, device="cuda")))
+    outs = lb.gemm_grouped(TBN, problems)
+    for s, c in enumerate(outs):
+        assert sha(host(c)) == golden_configs["c2"]["sha256"][s], s
+
+
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_grouped_mixed_shapes(lb, port, mode):
+    da, db = mode_dists(mode)
+    rng = np.random.default_rng(7 + mode)
+    problems, wants = [], []
+    for i in range(150):  # > 128: exercises the split into several launches
+        m, n, k = int(rng.integers(1, 200)), int(rng.integers(1, 100)), int(rng.integers(1, 700))
+        a = port.generate(da, 600 + mode, 2 * i, m, k)
+        b = port.generate(db, 600 + mode, 2 * i + 1, k, n)
+        ap = lb.encode_ternary(dev(a)) if a_mode_ternary(mode) else lb.encode_binary(dev(a))
+        bp = lb.encode_ternary(dev(b)) if b_mode_ternary(mode) else lb.encode_binary(dev(b))
+        problems.append((ap, lb.prepare_weights(lb.pack_b(bp)), torch.empty((m, n), dtype=torch.int16,
+                                                                            device="cuda")))
+        wants.append(port.gemm(mode, a, b))
+    outs = lb.gemm_grouped(mode, problems)
+    for got, want in zip(outs, wants):
+        assert (host(got) == want).all()
