@@ -270,8 +270,8 @@ def main():
     kernel = {"auto": lb.KERNEL_AUTO, "tensor": lb.KERNEL_TENSOR, "bitserial": lb.KERNEL_BITSERIAL}[args.kernel]
 
     mode, M, N, K, da, db, seed = CONFIGS[args.config]
-    r0 = M * rank // world
-    r1 = M * (rank + 1) // world
+    from paper_2205_09120_b200.shard import row_range
+    r0, r1 = row_range(M, rank, world)
     m = r1 - r0
 
     # ---- untimed setup: inputs in HBM, weights prepared ----
