@@ -245,6 +245,9 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "bitserial"])
+    ap.add_argument("--layout", default="lanes", choices=["lanes", "reference"],
+                    help="A plane layout written by the (untimed) encode: the B200 lane-interleaved layout or "
+                         "the reference bit order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-config side measurements")
@@ -276,7 +279,11 @@ def main():
 
     # ---- untimed setup: inputs in HBM, weights prepared ----
     a = lb.generate(da, seed, 0, m, K, row0=r0)
-    ap_ = lb.encode_binary(a) if mode == 0 else lb.encode_ternary(a)
+    layout = 1 if (args.layout == "lanes" and args.kernel != "bitserial") else 0
+    ap_ = lb.encode_binary(a, layout=layout) if mode == 0 else lb.encode_ternary(a, layout=layout)
+    ap_ref = None
+    if not args.no_e2e and layout != 0:  # the host drop-in exchanges reference-layout planes
+        ap_ref = lb.encode_binary(a) if mode == 0 else lb.encode_ternary(a)
     del a
     b = lb.generate(db, seed, 1, K, N)
     bp = lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)
@@ -324,11 +331,13 @@ def main():
     if not args.no_e2e:
         sb = (K + 7) // 8
         h_a0 = torch.empty((m, sb), dtype=torch.uint8, pin_memory=True)
-        h_a0.copy_(ap_.plane0[:, :sb])
+        src = ap_ref if ap_ref is not None else ap_
+        h_a0.copy_(src.plane0[:, :sb])
         h_a1 = None
-        if ap_.plane1 is not None:
+        if src.plane1 is not None:
             h_a1 = torch.empty((m, sb), dtype=torch.uint8, pin_memory=True)
-            h_a1.copy_(ap_.plane1[:, :sb])
+            h_a1.copy_(src.plane1[:, :sb])
+        del src
         h_pan = torch.empty(pb.panels.numel(), dtype=torch.uint8, pin_memory=True)
         h_pan.copy_(pb.panels)
         h_c = torch.empty((m, N), dtype=torch.int16, pin_memory=True)
@@ -363,6 +372,7 @@ def main():
         # sanity: e2e output equals the device-resident output
         assert torch.equal(h_c.cuda(), c), "e2e output differs from device path"
         del h_a0, h_a1, h_c
+        ap_ref = None
 
     pk = peaks()
     tensor_peak = 2.0 * pk["bf16_tflops"]  # dense int8 tcgen05 = 2x bf16 per SM-clock (4.5 vs 2.25 PF spec)
@@ -402,6 +412,7 @@ def main():
                                    f"A rows sharded over {world} GPU(s), B replicated",
                        "global_rows": M, "rows_per_rank": M // world, "l2": "flushed (256 MiB write) between steps",
                        "kernel": {1: "bitserial", 2: "tensor"}.get(chosen, str(chosen)),
+                       "a_layout": "lanes (B200 lane-interleaved bit planes from K1)" if layout else "reference",
                        "parallelism": f"row-shard x{world}"},
             "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "per_config": extra,

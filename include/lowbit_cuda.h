@@ -70,6 +70,16 @@ typedef enum lowbit_kernel {
 
 typedef void* lowbit_stream; /* cudaStream_t */
 
+/* Device plane layouts for the A operand.
+ * REFERENCE: the reference encoding, element t of a row at bit t%8 of byte
+ *            t/8 (core.hpp:3-10) — what the C++ API exchanges.
+ * LANES:     the B200 layout written by lowbit_encode_ex: within each 32-bit
+ *            word (32 consecutive elements) element j sits at bit
+ *            8*(j%4) + j/4, so the tensor-core kernel turns a word into int8
+ *            with one shift + mask per 4 elements.  A per-word bit
+ *            permutation: popcounts, pitch and padding rules are unchanged. */
+typedef enum lowbit_layout { LOWBIT_LAYOUT_REFERENCE = 0, LOWBIT_LAYOUT_LANES = 1 } lowbit_layout;
+
 /* ---- library / errors --------------------------------------------------- */
 int lowbit_abi_version(void);
 const char* lowbit_status_string(int status);
@@ -95,6 +105,11 @@ long long lowbit_plane_pitch(int cols);
  * NULL for ternary; it is only ever set, never cleared. */
 lowbit_status lowbit_encode(int ternary, const int8_t* values, int rows, int cols, long long ld, uint8_t* plane0,
                             uint8_t* plane1, long long pitch, int* zero_flag, lowbit_stream stream);
+
+/* encode with an explicit A layout (lowbit_layout). */
+lowbit_status lowbit_encode_ex(int ternary, int layout, const int8_t* values, int rows, int cols, long long ld,
+                               uint8_t* plane0, uint8_t* plane1, long long pitch, int* zero_flag,
+                               lowbit_stream stream);
 
 /* ---- K1b: pack_b (gemm.hpp:75-76; pack.cpp:64-127) ------------------------
  * b0/b1: K x N plane(s) packed along N (the reference B layout), row pitch
@@ -123,6 +138,13 @@ lowbit_status lowbit_prepare_weights(int ternary, const uint8_t* panels, int n, 
 lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int a_rows, int a_cols,
                           const void* weights, int b_ternary, int b_n, int b_k, int m, int n, int k, int k_blk,
                           int16_t* c, long long ldc, int kernel, lowbit_stream stream);
+
+/* lowbit_gemm with A planes in layout a_layout (lowbit_layout).  LANES
+ * planes are consumed by the tensor-core kernels only (the bit-serial kernel
+ * needs REFERENCE planes; LOWBIT_KERNEL_BITSERIAL + LANES is rejected). */
+lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch,
+                             int a_rows, int a_cols, const void* weights, int b_ternary, int b_n, int b_k, int m,
+                             int n, int k, int k_blk, int16_t* c, long long ldc, int kernel, lowbit_stream stream);
 
 /* The static per-shape kernel table behind LOWBIT_KERNEL_AUTO. */
 int lowbit_select_kernel(int mode, int m, int n, int k);
@@ -196,6 +218,11 @@ lowbit_status lowbit_pack_b_host(int ternary, const uint8_t* b0, const uint8_t* 
  * dist 0: uniform {-1,0,+1}; 1: uniform {-1,+1}; 2: P(0)=1/2, P(+-1)=1/4. */
 lowbit_status lowbit_generate(int dist, unsigned long long seed, int matrix_id, long long row0, long long rows,
                               long long cols, int8_t* out, lowbit_stream stream);
+
+/* ---- profiling experiments only ----------------------------------------
+ * Read-and-reset per-role cycle counters of the CTA-pair kernel (enabled by
+ * LOWBIT_DEBUG_PAIR=8 in the environment; see tools/pair_stats.py). */
+int lowbit_debug_pair_stats(unsigned long long* out16);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,8 @@ BNN, TNN, TBN = 0, 1, 2
 # lowbit_kernel
 KERNEL_AUTO, KERNEL_BITSERIAL, KERNEL_TENSOR, KERNEL_TENSOR_1CTA = 0, 1, 2, 3
 K_MAX16 = 32767
+# lowbit_layout
+LAYOUT_REFERENCE, LAYOUT_LANES = 0, 1
 
 
 # ---------------------------------------------------------------------------
@@ -103,6 +105,9 @@ SIGNATURES = {
     "lowbit_weights_bytes": (C.c_size_t, [_I, _I, _I]),
     "lowbit_prepare_weights": (_I, [_I, _P, _I, _I, _P, _P]),
     "lowbit_gemm": (_I, [_I, _P, _P, _LL, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _LL, _I, _P]),
+    "lowbit_encode_ex": (_I, [_I, _I, _P, _I, _I, _LL, _P, _P, _LL, _P, _P]),
+    "lowbit_gemm_ex": (_I, [_I, _I, _P, _P, _LL, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _LL, _I, _P]),
+    "lowbit_debug_pair_stats": (_I, [C.POINTER(C.c_ulonglong)]),
     "lowbit_select_kernel": (_I, [_I, _I, _I, _I]),
     "lowbit_gemm_lowbit_host": (_I, [_I, _P, _P, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P]),
     "lowbit_conv_rows": (_LL, [_I, _I, _I, _I, _I, _I, _I]),

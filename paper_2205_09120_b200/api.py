@@ -48,6 +48,7 @@ class Planes:
     cols: int
     plane0: torch.Tensor
     plane1: Optional[torch.Tensor]
+    layout: int = 0  # lowbit_layout: 0 reference bit order, 1 B200 lane-interleaved
 
     @property
     def ternary(self) -> bool:
@@ -87,29 +88,31 @@ def empty_planes(rows: int, cols: int, ternary: bool, device="cuda") -> Planes:
     return Planes(rows, cols, p0, p1)
 
 
-def _encode(values: torch.Tensor, ternary: bool, check_zero: bool = True) -> Planes:
+def _encode(values: torch.Tensor, ternary: bool, check_zero: bool = True, layout: int = 0) -> Planes:
     if values.dtype != torch.int8 or not values.is_cuda or values.dim() != 2:
         raise L.InvalidArgument("encode: expected a 2-D int8 CUDA tensor")
     if values.stride(1) != 1:
         values = values.contiguous()
     rows, cols = values.shape
     out = empty_planes(rows, cols, ternary, values.device)
+    out.layout = layout
     flag = torch.zeros(1, dtype=torch.int32, device=values.device)
-    L.check(L.lib.lowbit_encode(int(ternary), _ptr(values), rows, cols, values.stride(0), _ptr(out.plane0),
-                                _ptr(out.plane1), out.pitch, _ptr(flag), _stream()), "encode")
+    L.check(L.lib.lowbit_encode_ex(int(ternary), layout, _ptr(values), rows, cols, values.stride(0),
+                                   _ptr(out.plane0), _ptr(out.plane1), out.pitch, _ptr(flag), _stream()), "encode")
     if not ternary and check_zero and rows and cols and int(flag.item()):
         raise L.ZeroInBinaryInput("binary matrix contains a zero element")
     return out
 
 
-def encode_binary(values: torch.Tensor, check_zero: bool = True) -> Planes:
-    """core.cpp:13-28 (+1 -> 0, -1 -> 1; a 0 raises ZeroInBinaryInput)."""
-    return _encode(values, False, check_zero)
+def encode_binary(values: torch.Tensor, check_zero: bool = True, layout: int = 0) -> Planes:
+    """core.cpp:13-28 (+1 -> 0, -1 -> 1; a 0 raises ZeroInBinaryInput).
+    layout=1 writes the B200 lane-interleaved planes (tensor-core kernels only)."""
+    return _encode(values, False, check_zero, layout)
 
 
-def encode_ternary(values: torch.Tensor) -> Planes:
+def encode_ternary(values: torch.Tensor, layout: int = 0) -> Planes:
     """core.cpp:40-58 (plus plane, minus plane)."""
-    return _encode(values, True)
+    return _encode(values, True, True, layout)
 
 
 def pack_b(b: Planes) -> PackedB:
@@ -144,9 +147,9 @@ def gemm_lowbit(mode: int, a: Planes, b: Union[PackedB, Weights], dims, k_blk: i
         if st not in (L.OK, L.INVALID_ARGUMENT):
             L.check(st, "gemm_lowbit")
         w = prepare_weights(b)
-    L.check(L.lib.lowbit_gemm(mode, _ptr(a.plane0), _ptr(a.plane1), a.pitch, a.rows, a.cols, _ptr(w.buf),
-                              int(w.ternary), w.n, w.k, m, n, k, k_blk, _ptr(out), out.stride(0), kernel,
-                              _stream()), "gemm_lowbit")
+    L.check(L.lib.lowbit_gemm_ex(mode, a.layout, _ptr(a.plane0), _ptr(a.plane1), a.pitch, a.rows, a.cols,
+                                 _ptr(w.buf), int(w.ternary), w.n, w.k, m, n, k, k_blk, _ptr(out), out.stride(0),
+                                 kernel, _stream()), "gemm_lowbit")
     return out
 
 

@@ -11,10 +11,10 @@ namespace lb {
 lowbit_status launch_bitserial(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                                int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                                cudaStream_t stream);
-lowbit_status launch_tensor_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m,
+lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m,
                                  int n, int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                                  cudaStream_t stream);
-lowbit_status launch_tensor(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+lowbit_status launch_tensor(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                             int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                             cudaStream_t stream);
 }  // namespace lb
@@ -133,6 +133,14 @@ extern "C" int lowbit_select_kernel(int mode, int m, int n, int k) {
 extern "C" lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int a_rows,
                                      int a_cols, const void* weights, int b_ternary, int b_n, int b_k, int m, int n,
                                      int k, int k_blk, int16_t* c, long long ldc, int kernel, lowbit_stream stream) {
+    return lowbit_gemm_ex(mode, LOWBIT_LAYOUT_REFERENCE, a0, a1, a_pitch, a_rows, a_cols, weights, b_ternary, b_n,
+                          b_k, m, n, k, k_blk, c, ldc, kernel, stream);
+}
+
+extern "C" lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a0, const uint8_t* a1,
+                                        long long a_pitch, int a_rows, int a_cols, const void* weights, int b_ternary,
+                                        int b_n, int b_k, int m, int n, int k, int k_blk, int16_t* c, long long ldc,
+                                        int kernel, lowbit_stream stream) {
     const bool a_ternary = a1 != nullptr;
     lowbit_status st = validate_gemm(mode, a_ternary, b_ternary, a_rows, a_cols, b_n, b_k, m, n, k, k_blk);
     if (st) return st;
@@ -143,14 +151,19 @@ extern "C" lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t*
     if ((reinterpret_cast<uintptr_t>(weights) & 255))
         return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: weights must be 256-byte aligned");
     if (ldc < n) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: ldc < n");
+    if (a_layout != LOWBIT_LAYOUT_REFERENCE && a_layout != LOWBIT_LAYOUT_LANES)
+        return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown A plane layout");
     if (kernel == LOWBIT_KERNEL_AUTO) kernel = lowbit_select_kernel(mode, m, n, k);
     cudaStream_t s = (cudaStream_t)stream;
-    if (kernel == LOWBIT_KERNEL_BITSERIAL)
+    if (kernel == LOWBIT_KERNEL_BITSERIAL) {
+        if (a_layout != LOWBIT_LAYOUT_REFERENCE)
+            return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: the bit-serial kernel reads REFERENCE-layout planes");
         return lb::launch_bitserial(mode, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    }
     if (kernel == LOWBIT_KERNEL_TENSOR && m > 128)
-        return lb::launch_tensor_pair(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+        return lb::launch_tensor_pair(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     if (kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_1CTA)
-        return lb::launch_tensor(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+        return lb::launch_tensor(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown kernel id");
 }
 

@@ -64,6 +64,25 @@ LB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+// Blocking wait that parks the warp in the barrier unit (suspend-time hint)
+// instead of re-polling: a waiting warp is woken by the phase flip, so it no
+// longer burns issue slots that the ALU-heavy converter warps of the same
+// SMSP need (profiles/r01: polling loops were ~35% of issued instructions).
+LB_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
+LB_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait_sleep(bar, parity)) {
+    }
+}
 
 // ---------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor), tensor maps passed as __grid_constant__

@@ -14,6 +14,8 @@
 namespace lb {
 
 // One thread -> one 32-bit word of every plane of one row (32 values).
+// LAYOUT 0: the reference LSB-first layout; 1: the lane-interleaved B200 layout.
+template <int LAYOUT>
 __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, int rows, int cols, long long ld,
                               uint8_t* __restrict__ plane0, uint8_t* __restrict__ plane1, long long pitch,
                               int* zero_flag) {
@@ -28,8 +30,13 @@ __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, in
         uint32_t minus = 0, plus = 0;
         if (c0 < cols) {
             const int nvals = cols - c0 < 32 ? cols - c0 : 32;
-            encode_word32(values + r * ld + c0, nvals, plus, minus);
-            if (!ternary && ((plus | minus) != valid_mask32(nvals))) saw_zero = true;
+            if (LAYOUT == 0) {
+                encode_word32(values + r * ld + c0, nvals, plus, minus);
+                if (!ternary && ((plus | minus) != valid_mask32(nvals))) saw_zero = true;
+            } else {
+                encode_word32_lanes(values + r * ld + c0, nvals, plus, minus);
+                if (!ternary && ((plus | minus) != valid_mask32_lanes(nvals))) saw_zero = true;
+            }
         }
         uint32_t* d0 = reinterpret_cast<uint32_t*>(plane0 + r * pitch);
         if (ternary) {
@@ -206,6 +213,15 @@ using namespace lb;
 extern "C" lowbit_status lowbit_encode(int ternary, const int8_t* values, int rows, int cols, long long ld,
                                        uint8_t* plane0, uint8_t* plane1, long long pitch, int* zero_flag,
                                        lowbit_stream stream) {
+    return lowbit_encode_ex(ternary, LOWBIT_LAYOUT_REFERENCE, values, rows, cols, ld, plane0, plane1, pitch,
+                            zero_flag, stream);
+}
+
+extern "C" lowbit_status lowbit_encode_ex(int ternary, int layout, const int8_t* values, int rows, int cols,
+                                          long long ld, uint8_t* plane0, uint8_t* plane1, long long pitch,
+                                          int* zero_flag, lowbit_stream stream) {
+    if (layout != LOWBIT_LAYOUT_REFERENCE && layout != LOWBIT_LAYOUT_LANES)
+        return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "encode: unknown plane layout");
     if (rows < 0 || cols < 0) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "encode: negative shape");
     if (rows == 0 || cols == 0) return LOWBIT_OK;
     if (!values || !plane0 || (ternary && !plane1))
@@ -214,8 +230,12 @@ extern "C" lowbit_status lowbit_encode(int ternary, const int8_t* values, int ro
         (ternary && (reinterpret_cast<uintptr_t>(plane1) & 3)))
         return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "encode: pitch must be >= ceil(cols/8) and 4-byte aligned");
     const long long work = (long long)rows * (pitch / 4);
-    encode_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ternary, values, rows, cols, ld, plane0,
-                                                                          plane1, pitch, zero_flag);
+    if (layout == LOWBIT_LAYOUT_REFERENCE)
+        encode_kernel<0><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ternary, values, rows, cols, ld,
+                                                                                 plane0, plane1, pitch, zero_flag);
+    else
+        encode_kernel<1><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ternary, values, rows, cols, ld,
+                                                                                 plane0, plane1, pitch, zero_flag);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

@@ -32,6 +32,46 @@ __device__ __forceinline__ void encode_word32(const int8_t* src, int nvals, uint
     }
 }
 
+// Same as encode_word32 but producing the lane-interleaved layout
+// (element j -> bit 8*(j%4) + j/4, see expand.cuh).  With 4 values per
+// 32-bit lane word x_i (values 4i..4i+3), the per-byte flags of x_i land in
+// bit i of each byte: word |= flags_i << i.
+__device__ __forceinline__ void encode_word32_lanes(const int8_t* src, int nvals, uint32_t& plus, uint32_t& minus) {
+    plus = 0;
+    minus = 0;
+    uint32_t v[8];
+    if (nvals == 32 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
+        const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+        v[0] = lo.x, v[1] = lo.y, v[2] = lo.z, v[3] = lo.w, v[4] = hi.x, v[5] = hi.y, v[6] = hi.z, v[7] = hi.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = 4 * i + b;
+                if (j < nvals) x |= (uint32_t)(uint8_t)src[j] << (8 * b);
+            }
+            v[i] = x;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t neg = (v[i] >> 7) & 0x01010101u;
+        const uint32_t nz = nonzero_msb(v[i]) >> 7;
+        minus |= neg << i;
+        plus |= (nz & ~neg) << i;
+    }
+}
+
+// Bit mask of the first nvals elements in the lane-interleaved layout.
+__device__ __forceinline__ uint32_t valid_mask32_lanes(int nvals) {
+    uint32_t m = 0;
+    for (int j = 0; j < nvals && j < 32; ++j) m |= 1u << (8 * (j & 3) + (j >> 2));
+    return m;
+}
+
 inline int grid_for(long long work, int threads) {
     long long g = (work + threads - 1) / threads;
     const long long cap = 148LL * 16;  // 16 resident 256-thread blocks per SM

@@ -65,4 +65,84 @@ __device__ __forceinline__ void expand_row(uint32_t raw_p, uint32_t raw_m, uint3
     expand_word<A_TER, DBG>(p.w, m.w, row, r & 7, 6);
 }
 
+// ---------------------------------------------------------------------------
+// B200 ("lane-interleaved") plane layout, produced by lowbit_encode_ex with
+// LOWBIT_LAYOUT_LANES: within each 32-bit word (32 consecutive depth
+// positions) element j sits at bit 8*(j%4) + j/4, i.e. byte b holds elements
+// b, b+4, ..., b+28.  Expanding to int8 is then a shift and a mask per output
+// word: bytes of ((w >> q) & 0x01010101) are elements 4q..4q+3 in order.
+// Popcounts of whole words are unchanged by the permutation.
+// ---------------------------------------------------------------------------
+template <bool A_TER>
+__device__ __forceinline__ void expand_word_lanes(uint32_t pw, uint32_t mw, uint32_t row, int sw, int ch0) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int q = 4 * c + j;
+            const uint32_t P = (pw >> q) & 0x01010101u;
+            if (A_TER) {
+                const uint32_t M = (mw >> q) & 0x01010101u;
+                w[j] = M * 0xFFu + P;  // +1 -> 0x01, -1 -> 0xFF, 0 -> 0x00
+            } else {
+                w[j] = P * 0xFEu + 0x01010101u;  // bit 1 -> 0xFF (-1), bit 0 -> 0x01 (+1)
+            }
+        }
+        const int ch = ch0 + c;
+        sts_v4(row + ((ch ^ sw) << 4), w[0], w[1], w[2], w[3]);
+    }
+}
+
+template <bool A_TER, int LAYOUT>
+__device__ __forceinline__ void expand_half_layout(uint32_t raw_p, uint32_t raw_m, uint32_t a_tile, int r, int h) {
+    if (LAYOUT == 0) {
+        expand_half<A_TER>(raw_p, raw_m, a_tile, r, h);
+        return;
+    }
+    const uint2 p = lds_v2(raw_p + r * 16 + 8 * h);
+    uint2 m = make_uint2(0, 0);
+    if (A_TER) m = lds_v2(raw_m + r * 16 + 8 * h);
+    const uint32_t row = a_tile + r * 128;
+    expand_word_lanes<A_TER>(p.x, m.x, row, r & 7, 4 * h);
+    expand_word_lanes<A_TER>(p.y, m.y, row, r & 7, 4 * h + 2);
+}
+
+template <bool A_TER, int LAYOUT>
+__device__ __forceinline__ void expand_row_layout(uint32_t raw_p, uint32_t raw_m, uint32_t a_tile, int r) {
+    if (LAYOUT == 0) {
+        expand_row<A_TER>(raw_p, raw_m, a_tile, r);
+        return;
+    }
+    const uint4 p = lds_v4(raw_p + r * 16);
+    uint4 m = make_uint4(0, 0, 0, 0);
+    if (A_TER) m = lds_v4(raw_m + r * 16);
+    const uint32_t row = a_tile + r * 128;
+    expand_word_lanes<A_TER>(p.x, m.x, row, r & 7, 0);
+    expand_word_lanes<A_TER>(p.y, m.y, row, r & 7, 2);
+    expand_word_lanes<A_TER>(p.z, m.z, row, r & 7, 4);
+    expand_word_lanes<A_TER>(p.w, m.w, row, r & 7, 6);
+}
+
+// Timing experiment helper: the expansion ALU work on register-resident data,
+// stores suppressed (never-true guard keeps the work alive).
+template <bool A_TER, int LAYOUT>
+__device__ __forceinline__ void expand_row_regs(uint32_t seed_p, uint32_t seed_m, uint32_t a_tile, int r) {
+    const uint32_t row = a_tile + r * 128;
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi) {
+        const uint32_t pw = seed_p * (wi + 1), mw = seed_m * (wi + 3);
+        if (LAYOUT == 0) expand_word<A_TER, 2>(pw, mw & ~pw, row, r & 7, 2 * wi);
+        else {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t P = (pw >> q) & 0x01010101u, M = (mw >> q) & 0x01010101u;
+                acc ^= A_TER ? M * 0xFFu + P : P * 0xFEu + 0x01010101u;
+            }
+            if (acc == 0x9E3779B9u && pw == 0x7F4A7C15u) sts_v4(row, acc, 0, 0, 0);
+        }
+    }
+}
+
 }  // namespace lb

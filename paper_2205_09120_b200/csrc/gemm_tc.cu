@@ -42,7 +42,7 @@ struct TcParams {
     int16_t* c;
 };
 
-template <bool A_TER>
+template <bool A_TER, int LAYOUT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
                    const __grid_constant__ CUtensorMap tmap_a1, const TcParams prm) {
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int kb = 0; kb < prm.kblocks; ++kb) {
                 mbar_wait(&tma_full[stage], phase);
                 const uint32_t raw = sRaw_u + stage * 2 * TC_RAW_BYTES;
-                expand_half<A_TER>(raw, raw + TC_RAW_BYTES, sA_u + stage * TC_A_BYTES, r, h);
+                expand_half_layout<A_TER, LAYOUT>(raw, raw + TC_RAW_BYTES, sA_u + stage * TC_A_BYTES, r, h);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_ready[stage]);
@@ -212,7 +212,21 @@ static int pick_bn(int n) {
     return (n + 31) / 32 * 32;
 }
 
-lowbit_status launch_tensor(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+template <bool A_TER, int LAYOUT>
+static lowbit_status launch_tc_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
+                                       const TcParams& prm, int grid, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<A_TER, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TC_SMEM_BYTES));
+        attr = true;
+    }
+    gemm_tc_kernel<A_TER, LAYOUT><<<grid, TC_THREADS, TC_SMEM_BYTES, stream>>>(mb, ma0, ma1, prm);
+    LB_CUDA_TRY(cudaGetLastError());
+    return LOWBIT_OK;
+}
+
+lowbit_status launch_tensor(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                             int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                             cudaStream_t stream) {
     const WeightsLayout L(b_ternary, n, k);
@@ -243,25 +257,11 @@ lowbit_status launch_tensor(int a_ternary, const uint8_t* a0, const uint8_t* a1,
 
     const int tiles = prm.m_tiles * prm.n_tiles;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    if (a_ternary) {
-        static bool attr = false;
-        if (!attr) {
-            LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             TC_SMEM_BYTES));
-            attr = true;
-        }
-        gemm_tc_kernel<true><<<grid, TC_THREADS, TC_SMEM_BYTES, stream>>>(mb, ma0, ma1, prm);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             TC_SMEM_BYTES));
-            attr = true;
-        }
-        gemm_tc_kernel<false><<<grid, TC_THREADS, TC_SMEM_BYTES, stream>>>(mb, ma0, ma1, prm);
-    }
-    LB_CUDA_TRY(cudaGetLastError());
-    return LOWBIT_OK;
+    if (a_ternary)
+        return layout ? launch_tc_variant<true, 1>(mb, ma0, ma1, prm, grid, stream)
+                      : launch_tc_variant<true, 0>(mb, ma0, ma1, prm, grid, stream);
+    return layout ? launch_tc_variant<false, 1>(mb, ma0, ma1, prm, grid, stream)
+                  : launch_tc_variant<false, 0>(mb, ma0, ma1, prm, grid, stream);
 }
 
 }  // namespace lb

@@ -327,3 +327,72 @@ def test_grouped_mixed_shapes(lb, port, mode):
     outs = lb.gemm_grouped(mode, problems)
     for got, want in zip(outs, wants):
         assert (host(got) == want).all()
+
+
+# ------------------------------------------------------------------ B200 lane-interleaved A layout
+def to_lanes(planes: np.ndarray) -> np.ndarray:
+    """Reference-layout plane rows -> LOWBIT_LAYOUT_LANES (element j of each
+    32-bit word moves from bit j to bit 8*(j%4) + j//4)."""
+    rows, sb = planes.shape
+    padded = np.zeros((rows, (sb + 3) // 4 * 4), np.uint8)
+    padded[:, :sb] = planes
+    words = padded.view("<u4").astype(np.uint64)
+    out = np.zeros_like(words)
+    for j in range(32):
+        out |= ((words >> j) & 1) << (8 * (j % 4) + j // 4)
+    return out.astype("<u4").view(np.uint8)[:, :sb]
+
+
+@pytest.mark.parametrize("shape", [(1, 8), (7, 13), (33, 129), (257, 1000), (5, 2048)])
+def test_encode_lanes_layout(lb, port, shape):
+    rows, cols = shape
+    for tern in (False, True):
+        v = port.generate(0 if tern else 1, 21, int(tern), rows, cols)
+        w0, w1 = port.encode(v, tern)
+        got = (lb.encode_ternary(dev(v), layout=1) if tern else lb.encode_binary(dev(v), layout=1))
+        sb = (cols + 7) // 8
+        assert (host(got.plane0)[:, :sb] == to_lanes(w0)).all()
+        if tern:
+            assert (host(got.plane1)[:, :sb] == to_lanes(w1)).all()
+    with pytest.raises(lb.ZeroInBinaryInput):
+        lb.encode_binary(torch.zeros((2, 40), dtype=torch.int8, device="cuda"), layout=1)
+
+
+@pytest.mark.parametrize("kernel", [2, 3])
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_gemm_lanes_layout(lb, port, mode, kernel):
+    da, db = mode_dists(mode)
+    for i, (m, n, k) in enumerate([(1, 1, 1), (17, 9, 500), (70, 25, 7), (360, 96, 256), (300, 520, 1000),
+                                   (129, 257, 4100), (1000, 300, 2048)]):
+        a = port.generate(da, 88 + i, 0, m, k)
+        b = port.generate(db, 88 + i, 1, k, n)
+        ap = lb.encode_ternary(dev(a), layout=1) if a_mode_ternary(mode) else lb.encode_binary(dev(a), layout=1)
+        bp = lb.encode_ternary(dev(b)) if b_mode_ternary(mode) else lb.encode_binary(dev(b))
+        got = host(lb.gemm_lowbit(mode, ap, lb.prepare_weights(lb.pack_b(bp)), (m, n, k), kernel=kernel))
+        assert (got == port.gemm(mode, a, b)).all(), (mode, m, n, k)
+
+
+def test_lanes_layout_rejected_by_bitserial(lb, port):
+    ap = lb.encode_ternary(dev(port.generate(0, 3, 0, 16, 64)), layout=1)
+    w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(dev(port.generate(0, 3, 1, 64, 8)))))
+    with pytest.raises(lb.InvalidArgument):
+        lb.gemm_lowbit(TNN, ap, w, (16, 8, 64), kernel=1)
+
+
+def test_config5_lanes_hash(lb, golden_configs):
+    m, n, k = 1048576, 1024, 2048
+    a = lb.generate(0, 47, 0, m, k)
+    ap = lb.encode_ternary(a, layout=1)
+    del a
+    w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(lb.generate(0, 47, 1, k, n))))
+    c = lb.gemm_lowbit(TNN, ap, w, (m, n, k), kernel=2)
+    assert sha(host(c)) == golden_configs["c5"]["sha256"]
+
+
+def test_config3_lanes_hash(lb, golden_configs):
+    m = n = 8192
+    k = 4096
+    ap = lb.encode_binary(lb.generate(1, 45, 0, m, k), layout=1)
+    w = lb.prepare_weights(lb.pack_b(lb.encode_binary(lb.generate(1, 45, 1, k, n))))
+    c = lb.gemm_lowbit(BNN, ap, w, (m, n, k), kernel=2)
+    assert sha(host(c)) == golden_configs["c3"]["sha256"]
