@@ -516,7 +516,10 @@ def side_configs(lb, torch, flush, pk):
     for kn, kid in kernels:
         ms = time_device(torch, lambda: lb.conv2d_lowbit(1, fm, False, w, 3, 3, 1, 1, kernel=kid, out=o,
                                                          workspace=wsp), flush)
-        res[kn] = {"ms": ms, "TOPS": ops4 / (ms * 1e-3) / 1e12}
+        res[kn] = {"ms": ms, "TOPS": ops4 / (ms * 1e-3) / 1e12, "frac": ops4 / (ms * 1e-3) / 1e12 /
+                   (tensor_peak if kn == "tensor" else popc(1)),
+                   "path": ("implicit GeMM: im2col TMA -> tcgen05 (no bit planes)" if kn == "tensor"
+                            else "K4 fused im2col+encode -> K2 bit-serial")}
     # K4 alone (HBM-bound): int8 NHWC in, two bit planes out
     pitch = lb.plane_pitch(1152)
     p0 = wsp[: 200704 * pitch]
@@ -532,8 +535,16 @@ def side_configs(lb, torch, flush, pk):
     res["k4_encode"] = {"ms": ms, "GB/s": k4_bytes / (ms * 1e-3) / 1e9,
                         "frac_hbm": k4_bytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": k4_bytes}
     out["c4"] = res
-    # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
+    # c5 "from int8 A": the int8 sign matrix straight to the tensor cores (no encode)
     a = lb.generate(0, 47, 0, 1048576, 2048)
+    w5 = lb.prepare_weights(lb.pack_b(lb.encode_ternary(lb.generate(0, 47, 1, 2048, 1024))))
+    c5 = torch.empty((1048576, 1024), dtype=torch.int16, device="cuda")
+    ms = time_device(torch, lambda: lb.gemm_lowbit_i8(1, a, w5, (1048576, 1024, 2048), out=c5), flush, reps=10)
+    ops5 = 2.0 * 1048576 * 1024 * 2048
+    out["c5_from_int8"] = {"ms": ms, "TOPS": ops5 / (ms * 1e-3) / 1e12, "frac": ops5 / (ms * 1e-3) / 1e12 / tensor_peak,
+                           "path": "lowbit_gemm_i8: int8 A tiles by TMA (128B swizzle) -> tcgen05 kind::i8"}
+    del c5, w5
+    # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
     planes = lb.empty_planes(1048576, 2048, True)
     enc = lambda: L.check(L.lib.lowbit_encode(1, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,
                                               C.c_void_p(planes.plane0.data_ptr()),

@@ -146,6 +146,15 @@ lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a0, const ui
                              int a_rows, int a_cols, const void* weights, int b_ternary, int b_n, int b_k, int m,
                              int n, int k, int k_blk, int16_t* c, long long ldc, int kernel, lowbit_stream stream);
 
+/* gemm_lowbit with A given as dense int8 sign values (row stride lda bytes,
+ * lda % 16 == 0): the "from int8 A" form.  Values must be in {-1, 0, +1}
+ * ({-1, +1} for BNN), the SignMatrix contract (core.hpp:21-33); the operand
+ * kind follows the mode.  TMA feeds the tensor cores directly — no encode,
+ * no converters.  Same validation and results as lowbit_gemm. */
+lowbit_status lowbit_gemm_i8(int mode, const int8_t* a, long long lda, int a_rows, int a_cols, const void* weights,
+                             int b_ternary, int b_n, int b_k, int m, int n, int k, int k_blk, int16_t* c,
+                             long long ldc, lowbit_stream stream);
+
 /* The static per-shape kernel table behind LOWBIT_KERNEL_AUTO. */
 int lowbit_select_kernel(int mode, int m, int n, int k);
 
@@ -186,7 +195,11 @@ lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t
  * (ChannelOverflow, weight shape, modes, EmptyOutput), K4, then lowbit_gemm
  * into out = int16 NHWC [batch][OH][OW][cout].  fm_binary is the feature
  * map's Mode (binary maps pad with binary_pad_value, ternary maps with 0);
- * a 0 in the A operand of a BNN conv sets *zero_flag. */
+ * a 0 in the A operand of a BNN conv sets *zero_flag.
+ * TNN/TBN convs whose padding reads as 0 and whose c is a multiple of 128
+ * run as an implicit GeMM: an im2col TMA map feeds the int8 activations
+ * (values in {-1,0,+1}, the FeatureMap contract) straight to the tensor
+ * cores, workspace unused.  Other convs go through lowbit_conv_encode. */
 long long lowbit_conv_rows(int batch, int h, int w, int kh, int kw, int stride, int padding);
 lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int batch, int h, int w, int c, int kh, int kw,
                                  int stride, int padding, int pad_value, uint8_t* plane0, uint8_t* plane1,

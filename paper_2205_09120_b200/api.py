@@ -224,3 +224,18 @@ def gemm_grouped(mode: int, problems, b_ternary: Optional[bool] = None):
                                w.buf.data_ptr(), a.rows, w.n, a.cols, out.data_ptr(), out.stride(0))
     L.check(L.lib.lowbit_gemm_grouped(mode, int(b_ternary), len(problems), arr, _stream()), "gemm_grouped")
     return [p[2] for p in problems]
+
+
+def gemm_lowbit_i8(mode: int, a: torch.Tensor, w: Weights, dims, k_blk: int = 4096,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """gemm_lowbit from dense int8 sign values (the "from int8 A" form):
+    TMA feeds the tensor cores directly, no encode.  a: int8 [m, k] CUDA, rows
+    16-byte aligned."""
+    m, n, k = dims
+    if a.dtype != torch.int8 or not a.is_cuda or a.dim() != 2 or a.stride(1) != 1:
+        raise L.InvalidArgument("gemm_lowbit_i8: expected a row-major 2-D int8 CUDA tensor")
+    if out is None:
+        out = torch.empty((max(m, 1), max(n, 1)), dtype=torch.int16, device=a.device)
+    L.check(L.lib.lowbit_gemm_i8(mode, _ptr(a), a.stride(0), a.shape[0], a.shape[1], _ptr(w.buf), int(w.ternary),
+                                 w.n, w.k, m, n, k, k_blk, _ptr(out), out.stride(0), _stream()), "gemm_lowbit_i8")
+    return out

@@ -14,6 +14,8 @@ lowbit_status launch_bitserial(int mode, const uint8_t* a0, const uint8_t* a1, l
 lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m,
                                  int n, int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                                  cudaStream_t stream);
+lowbit_status launch_tensor_pair_i8(const int8_t* a, long long lda, int m, int n, int k, const void* weights,
+                                    int b_ternary, int16_t* c, long long ldc, cudaStream_t stream);
 lowbit_status launch_tensor(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                             int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                             cudaStream_t stream);
@@ -117,8 +119,8 @@ static lowbit_status validate_gemm(int mode, bool a_ternary, int b_ternary, int 
 //   c1 360x96x256      tcgen05 6.7 us   vs bit-serial 12.6 us (graph replay)
 //   c2 sweep (64)      tcgen05 5.0 us   vs bit-serial 10.5 us per shape
 //   c3 8192^2x4096     tcgen05 2.68 POPS vs bit-serial 0.28 POPS (95% of POPC peak)
-//   c4 conv            tcgen05 0.38 POPS vs bit-serial 0.09 POPS
-//   c5 1Mx1024x2048    tcgen05 2.5 POPS
+//   c4 conv            tcgen05 implicit GeMM 48 us (1.23 POPS) vs K4 + bit-serial 630 us
+//   c5 1Mx1024x2048    tcgen05 2.55-2.69 POPS from bit planes, 3.15 POPS from int8
 // The int8 tensor path wins every measured shape, including the launch-bound
 // ones, so AUTO maps to it; the bit-serial kernel stays selectable (and is the
 // one the grouped small-GeMM launch uses, lowbit_gemm_grouped).
@@ -165,6 +167,21 @@ extern "C" lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a
     if (kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_1CTA)
         return lb::launch_tensor(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown kernel id");
+}
+
+extern "C" lowbit_status lowbit_gemm_i8(int mode, const int8_t* a, long long lda, int a_rows, int a_cols,
+                                        const void* weights, int b_ternary, int b_n, int b_k, int m, int n, int k,
+                                        int k_blk, int16_t* c, long long ldc, lowbit_stream stream) {
+    // the A operand kind follows the mode (BNN binary, TNN/TBN ternary)
+    lowbit_status st = validate_gemm(mode, mode != LOWBIT_BNN, b_ternary, a_rows, a_cols, b_n, b_k, m, n, k, k_blk);
+    if (st) return st;
+    if (!a || !weights || !c) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm_i8: NULL pointer");
+    if ((lda & 15) || lda < k || (reinterpret_cast<uintptr_t>(a) & 15))
+        return set_error(LOWBIT_INVALID_ARGUMENT, "gemm_i8: A rows must be 16-byte aligned (lda % 16 == 0)");
+    if ((reinterpret_cast<uintptr_t>(weights) & 255))
+        return set_error(LOWBIT_INVALID_ARGUMENT, "gemm_i8: weights must be 256-byte aligned");
+    if (ldc < n) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm_i8: ldc < n");
+    return lb::launch_tensor_pair_i8(a, lda, m, n, k, weights, b_ternary, c, ldc, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------

@@ -231,6 +231,15 @@ LB_DEV void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t lead
         "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
         : "memory");
 }
+// im2col-mode TMA (pair form): 4-D NHWC map {c, w, h, n} + filter-tap offsets.
+LB_DEV void tma_load_im2col_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c, int w, int h,
+                                    int n, uint16_t off_w, uint16_t off_h) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+        : "memory");
+}
 template <uint32_t kCols>
 LB_DEV void tmem_alloc_pair(uint32_t* dst_smem) {  // whole warp, same warp id in both CTAs
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),

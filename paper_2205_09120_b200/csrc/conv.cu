@@ -87,6 +87,12 @@ __global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict
 
 }  // namespace lb
 
+namespace lb {
+lowbit_status launch_conv_pair_im2col(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
+                                      int pad, const void* weights, int b_ternary, int cout, int16_t* out,
+                                      cudaStream_t stream);
+}
+
 using namespace lb;
 
 static int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
@@ -148,8 +154,20 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
                                        int16_t* out, int kernel, lowbit_stream stream) {
     lowbit_status st = validate_conv(mode, batch, h, w, c, fm_binary, b_ternary, cout, k, kh, kw, stride, padding);
     if (st) return st;
-    if (!workspace || !weights || !out) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d: NULL pointer");
+    if (!weights || !out) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d: NULL pointer");
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
+    // Implicit GeMM straight from the int8 feature map (TMA im2col -> UMMA, no
+    // bit planes, no workspace) whenever padding reads as 0 — ternary
+    // activations, or no padding — and the channel count tiles into 128-byte
+    // k-blocks.  BNN keeps the bit path: its padding is +-1 and a 0 activation
+    // must raise ZeroInBinaryInput (conv.cpp:13, core.cpp:23).
+    const bool pad_is_zero = padding == 0 || !fm_binary;
+    if (mode != LOWBIT_BNN && pad_is_zero && c % 128 == 0 && rows <= 0x7FFFFFFFLL &&
+        (kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) &&
+        (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0)
+        return lb::launch_conv_pair_im2col(fm, batch, h, w, c, kh, kw, stride, padding, weights, b_ternary, cout, out,
+                                           (cudaStream_t)stream);
+    if (!workspace) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d: NULL workspace");
     const long long pitch = lowbit_plane_pitch(k);
     uint8_t* p0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     const int a_binary = mode == LOWBIT_BNN;

@@ -62,6 +62,8 @@ struct PairParams {
     int16_t* c;
     int tma_store;
     int a_stages, b_stages, raw_stages;
+    // LAYOUT 3 (implicit-GeMM convolution): output geometry for the im2col TMA
+    int conv_ow, conv_ohw, conv_stride, conv_pad, conv_kw, conv_cblocks;
     int debug;  // timing experiments only (results invalid): 1 skip expansion, 2 ALU only, 3 stores only
 };
 
@@ -137,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 
     if (warp == PR_W_RAW) {
         // ===================== raw A-bit producer (both CTAs) =====================
-        if (lane == 0) {
+        if (LAYOUT < 2 && lane == 0) {
             const uint32_t raw_bytes = (A_TER ? 2 : 1) * PR_RAW_BYTES;
             uint32_t t = 0;  // k-block counter over the whole persistent loop
             for (int tile = pair; tile < num_tiles; tile += npairs) {
@@ -156,17 +158,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     } else if (warp == PR_W_B) {
         // ===================== B producer (both CTAs; bytes land on the leader) =====================
         if (lane == 0) {
-            const uint32_t b_bytes_pair = (uint32_t)bn * PR_BK;  // both CTAs' halves
+            // both CTAs' halves of B (+ both CTAs' int8 A tiles when A comes straight from TMA)
+            const uint32_t pair_bytes = (uint32_t)bn * PR_BK + (LAYOUT >= 2 ? 2 * PR_A_BYTES : 0);
             const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
             uint32_t t = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
                 const int brow = nt * bn + (int)rank * bnh;
+                const int arow = mt * 2 * PR_BM + (int)rank * PR_BM;
+                int img = 0, oy = 0, ox = 0;
+                if (LAYOUT == 3) {  // first output pixel of this CTA's 128 rows
+                    img = arow / prm.conv_ohw;
+                    const int rem = arow - img * prm.conv_ohw;
+                    oy = rem / prm.conv_ow;
+                    ox = rem - oy * prm.conv_ow;
+                }
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t st = t % PR_B_STAGES;
                     mbar_wait_sleep(&a_empty[st], ((t / PR_B_STAGES) & 1) ^ 1);  // shared ring: A/B slot free
-                    if (leader) mbar_arrive_expect_tx(&b_full[st], b_bytes_pair);
+                    if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
                     tma_load_2d_pair(smem_u32(sB + st * PR_B_BYTES), &tmap_b, b_full0 + st * 8, kb * PR_BK, brow);
+                    if (LAYOUT == 2) {  // dense int8 A: 128 rows x 128 depth, 128B swizzle = the UMMA tile
+                        tma_load_2d_pair(smem_u32(sA + st * PR_A_BYTES), &tmap_a0, b_full0 + st * 8, kb * PR_BK, arow);
+                    } else if (LAYOUT == 3) {  // implicit GeMM: tap (ky, kx), 128 channels, 128 output pixels
+                        const int tap = kb / prm.conv_cblocks, cb = kb - tap * prm.conv_cblocks;
+                        const int ky = tap / prm.conv_kw, kx = tap - ky * prm.conv_kw;
+                        tma_load_im2col_4d_pair(smem_u32(sA + st * PR_A_BYTES), &tmap_a0, b_full0 + st * 8, cb * 128,
+                                                ox * prm.conv_stride - prm.conv_pad, oy * prm.conv_stride - prm.conv_pad,
+                                                img, (uint16_t)kx, (uint16_t)ky);
+                    }
                 }
             }
         }
@@ -189,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * PR_MAX_BN;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t sa = t % PR_A_STAGES, sb = t % PR_B_STAGES;
-                    {
+                    if (LAYOUT < 2) {
                         PR_T0();
                         mbar_wait(&a_ready[sa], (t / PR_A_STAGES) & 1);  // latency-critical: poll
                         PR_ACC(w_a);
@@ -231,7 +251,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         const int r = threadIdx.x & 127;
         const uint32_t sA_u = smem_u32(sA), sRaw_u = smem_u32(sRaw);
         const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), 0);
-        const uint32_t total = (uint32_t)((num_tiles - pair + npairs - 1) / npairs) * (uint32_t)prm.kblocks;
+        const uint32_t total =
+            LAYOUT >= 2 ? 0u : (uint32_t)((num_tiles - pair + npairs - 1) / npairs) * (uint32_t)prm.kblocks;
         long long w_raw = 0, w_slot = 0, w_work = 0;
         const long long t_start = clock64();
         for (uint32_t t = g; t < total; t += 2) {
@@ -398,11 +419,9 @@ static lowbit_status launch_pair_variant(const CUtensorMap& mb, const CUtensorMa
     return LOWBIT_OK;
 }
 
-lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m,
-                                 int n, int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
-                                 cudaStream_t stream) {
+static PairParams pair_params(int m, int n, int k, int b_ternary, int16_t* c, long long ldc) {
     const WeightsLayout L(b_ternary, n, k);
-    PairParams prm;
+    PairParams prm{};
     prm.m = m;
     prm.n = n;
     prm.kblocks = L.kp / PR_BK;
@@ -420,11 +439,37 @@ lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, c
     prm.a_stages = PR_DEF_A_STAGES;
     prm.b_stages = PR_DEF_B_STAGES;
     prm.raw_stages = PR_DEF_RAW_STAGES;
+    return prm;
+}
 
-    CUtensorMap mb, ma0, ma1, mc;
-    if (!make_map_2d(&mb, weights, (uint64_t)L.kp, (uint64_t)L.np, (uint64_t)L.kp, PR_BK, (uint32_t)(prm.bn / 2),
+// B (weights) and C (TMA store) maps shared by every A mode.
+static lowbit_status pair_bc_maps(const PairParams& prm, int b_ternary, int k, const void* weights, CUtensorMap* mb,
+                                  CUtensorMap* mc) {
+    const WeightsLayout L(b_ternary, prm.n, k);
+    if (!make_map_2d(mb, weights, (uint64_t)L.kp, (uint64_t)L.np, (uint64_t)L.kp, PR_BK, (uint32_t)(prm.bn / 2),
                      CU_TENSOR_MAP_SWIZZLE_128B))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for B");
+    if (prm.tma_store &&
+        !make_map_2d(mc, prm.c, (uint64_t)prm.n, (uint64_t)prm.m, (uint64_t)prm.ldc * 2, 32, 32,
+                     CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_DATA_TYPE_UINT16))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for C");
+    if (!prm.tma_store) *mc = *mb;
+    return LOWBIT_OK;
+}
+
+static int pair_count(const PairParams& prm) {
+    const int tiles = prm.m_tiles * prm.n_tiles;
+    return tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+}
+
+// A as bit planes (LAYOUT 0 reference / 1 lanes), expanded by the converters.
+lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch,
+                                 int m, int n, int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                                 cudaStream_t stream) {
+    const PairParams prm = pair_params(m, n, k, b_ternary, c, ldc);
+    CUtensorMap mb, ma0, ma1, mc;
+    lowbit_status st = pair_bc_maps(prm, b_ternary, k, weights, &mb, &mc);
+    if (st) return st;
     if (!make_map_2d(&ma0, a0, (uint64_t)a_pitch, (uint64_t)m, (uint64_t)a_pitch, 16, PR_BM,
                      CU_TENSOR_MAP_SWIZZLE_NONE))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for A");
@@ -435,21 +480,47 @@ lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, c
     } else {
         ma1 = ma0;
     }
-    if (prm.tma_store) {
-        if (!make_map_2d(&mc, c, (uint64_t)n, (uint64_t)m, (uint64_t)ldc * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B,
-                         CU_TENSOR_MAP_DATA_TYPE_UINT16))
-            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for C");
-    } else {
-        mc = ma0;
-    }
-
-    const int tiles = prm.m_tiles * prm.n_tiles;
-    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    const int pairs = pair_count(prm);
     if (a_ternary)
         return layout ? launch_pair_variant<true, 1>(mb, ma0, ma1, mc, prm, pairs, stream)
                       : launch_pair_variant<true, 0>(mb, ma0, ma1, mc, prm, pairs, stream);
     return layout ? launch_pair_variant<false, 1>(mb, ma0, ma1, mc, prm, pairs, stream)
                   : launch_pair_variant<false, 0>(mb, ma0, ma1, mc, prm, pairs, stream);
+}
+
+// A as dense int8 sign values (LAYOUT 2): TMA brings UMMA-ready tiles, no converters.
+lowbit_status launch_tensor_pair_i8(const int8_t* a, long long lda, int m, int n, int k, const void* weights,
+                                    int b_ternary, int16_t* c, long long ldc, cudaStream_t stream) {
+    const PairParams prm = pair_params(m, n, k, b_ternary, c, ldc);
+    CUtensorMap mb, ma, mc;
+    lowbit_status st = pair_bc_maps(prm, b_ternary, k, weights, &mb, &mc);
+    if (st) return st;
+    if (!make_map_2d(&ma, a, (uint64_t)k, (uint64_t)m, (uint64_t)lda, PR_BK, PR_BM, CU_TENSOR_MAP_SWIZZLE_128B))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for int8 A");
+    return launch_pair_variant<true, 2>(mb, ma, ma, mc, prm, pair_count(prm), stream);
+}
+
+// Implicit-GeMM convolution (LAYOUT 3): NHWC int8 sign values through an im2col TMA map;
+// one k-block = one filter tap x 128 channels (requires c % 128 == 0).
+lowbit_status launch_conv_pair_im2col(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
+                                      int pad, const void* weights, int b_ternary, int cout, int16_t* out,
+                                      cudaStream_t stream) {
+    const int oh = (h + 2 * pad - kh) / stride + 1, ow = (w + 2 * pad - kw) / stride + 1;
+    const long long rows = (long long)batch * oh * ow;
+    const int k = kh * kw * cch;
+    PairParams prm = pair_params((int)rows, cout, k, b_ternary, out, cout);
+    prm.conv_ow = ow;
+    prm.conv_ohw = oh * ow;
+    prm.conv_stride = stride;
+    prm.conv_pad = pad;
+    prm.conv_kw = kw;
+    prm.conv_cblocks = cch / 128;
+    CUtensorMap mb, ma, mc;
+    lowbit_status st = pair_bc_maps(prm, b_ternary, k, weights, &mb, &mc);
+    if (st) return st;
+    if (!make_map_im2col(&ma, fm, batch, h, w, cch, kh, kw, stride, pad, 128, PR_BM, CU_TENSOR_MAP_SWIZZLE_128B))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeIm2col failed");
+    return launch_pair_variant<true, 3>(mb, ma, ma, mc, prm, pair_count(prm), stream);
 }
 
 }  // namespace lb

@@ -34,6 +34,33 @@ inline bool make_map_2d(CUtensorMap* map, const void* base, uint64_t dim0, uint6
     return r == CUDA_SUCCESS;
 }
 
+// 4-D NHWC int8 im2col map for implicit-GeMM convolution (fprop): lower
+// corner -pad, upper corner pad - (k-1), traversal stride = conv stride
+// (the CUTLASS convention, cutlass/conv/collective/detail.hpp).  Each load
+// brings `pixels` consecutive output pixels x `channels` channels of one
+// filter tap (given as the instruction's im2col offsets).
+inline bool make_map_im2col(CUtensorMap* map, const void* base, int n, int h, int w, int c, int kh, int kw,
+                            int stride, int pad, uint32_t channels, uint32_t pixels, CUtensorMapSwizzle swz) {
+    static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+    }
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)c, (cuuint64_t)w * c, (cuuint64_t)h * w * c};
+    int lower[2] = {-pad, -pad};
+    int upper[2] = {pad - (kw - 1), pad - (kh - 1)};
+    cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, lower, upper,
+                    channels, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 inline int num_sms() {
     static int sms = 0;
     if (!sms) {

@@ -94,3 +94,35 @@ def test_config4_full(lb, golden_configs):
         out = lb.conv2d_lowbit(TNN, fm, False, w, 3, 3, 1, 1, kernel=kernel)
         h = hashlib.sha256(out.cpu().numpy().astype("<i2").tobytes()).hexdigest()
         assert h == golden_configs["c4"]["sha256"], kernel
+
+
+@pytest.mark.parametrize("mode", [TNN, TBN])
+def test_conv_implicit_gemm_im2col(lb, port, mode):
+    """c % 128 == 0 and zero padding: the TMA-im2col implicit GeMM path."""
+    da, db = mode_dists(mode)
+    i = 0
+    for (batch, h, w, ch, ksz, stride, pad) in [(2, 9, 9, 128, 3, 1, 1), (3, 8, 7, 128, 3, 2, 1), (1, 5, 5, 256, 3, 1, 0),
+                                                (2, 6, 6, 128, 1, 1, 0), (1, 16, 16, 128, 3, 2, 0),
+                                                (4, 11, 13, 128, 3, 1, 1)]:
+        i += 1
+        fm = port.generate(0, 70 + i, 0, batch * h * w, ch).reshape(batch, h, w, ch)  # ternary map -> pad 0
+        wt = port.generate(db, 70 + i, 1, ksz * ksz * ch, 96)
+        wts = weights_for(lb, wt, mode)
+        for kernel in (0, 2):
+            got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), False, wts, ksz, ksz, stride, pad,
+                                   kernel=kernel).cpu().numpy()
+            for img in range(batch):
+                want = port.direct_conv(fm[img], False, wt, ksz, ksz, stride, pad)
+                assert (got[img].astype(np.int32) == want).all(), (mode, batch, h, w, ch, ksz, stride, pad, img)
+
+
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_gemm_from_int8(lb, port, mode):
+    da, db = mode_dists(mode)
+    for i, (m, n, k) in enumerate([(1, 1, 16), (17, 9, 512), (300, 520, 1008), (360, 96, 256), (129, 257, 4096),
+                                   (1000, 300, 2048)]):
+        a = port.generate(da, 90 + i, 0, m, k)
+        b = port.generate(db, 90 + i, 1, k, n)
+        bp = lb.encode_ternary(torch.from_numpy(b).cuda()) if mode == TNN else lb.encode_binary(torch.from_numpy(b).cuda())
+        got = lb.gemm_lowbit_i8(mode, torch.from_numpy(a).cuda(), lb.prepare_weights(lb.pack_b(bp)), (m, n, k))
+        assert (got.cpu().numpy() == port.gemm(mode, a, b)).all(), (mode, m, n, k)
