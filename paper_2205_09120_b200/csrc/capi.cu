@@ -203,7 +203,10 @@ struct Scratch {
     }
 };
 struct HostCtx {
+    static constexpr int kChunks = 8;
     Scratch a0, a1, panels, weights, c, vals, flag;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[kChunks] = {}, ev_c[kChunks] = {}, ev_w = nullptr, ev_done = nullptr;
 };
 thread_local HostCtx g_ctx;
 }  // namespace
@@ -229,27 +232,64 @@ extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, co
     LB_CUDA_TRY(X.panels.ensure(pbytes));
     LB_CUDA_TRY(X.weights.ensure(wbytes));
     LB_CUDA_TRY(X.c.ensure((size_t)m * n * sizeof(int16_t)));
-    if (pitch == hstride) {
-        LB_CUDA_TRY(cudaMemcpyAsync(X.a0.ptr, a0, abytes, cudaMemcpyHostToDevice, s));
-        if (a_ternary) LB_CUDA_TRY(cudaMemcpyAsync(X.a1.ptr, a1, abytes, cudaMemcpyHostToDevice, s));
-    } else {  // re-pitch to 16-byte rows; zero the padding first
-        LB_CUDA_TRY(cudaMemsetAsync(X.a0.ptr, 0, abytes, s));
-        LB_CUDA_TRY(cudaMemcpy2DAsync(X.a0.ptr, pitch, a0, hstride, hstride, m, cudaMemcpyHostToDevice, s));
-        if (a_ternary) {
-            LB_CUDA_TRY(cudaMemsetAsync(X.a1.ptr, 0, abytes, s));
-            LB_CUDA_TRY(cudaMemcpy2DAsync(X.a1.ptr, pitch, a1, hstride, hstride, m, cudaMemcpyHostToDevice, s));
-        }
-    }
+    // weights: upload + prepare once on the caller's stream
     LB_CUDA_TRY(cudaMemcpyAsync(X.panels.ptr, panels, pbytes, cudaMemcpyHostToDevice, s));
     if ((st = lowbit_prepare_weights(b_ternary, static_cast<const uint8_t*>(X.panels.ptr), n, k, X.weights.ptr,
                                      stream)))
         return st;
-    if ((st = lowbit_gemm(mode, static_cast<const uint8_t*>(X.a0.ptr),
-                          a_ternary ? static_cast<const uint8_t*>(X.a1.ptr) : nullptr, pitch, a_rows, a_cols,
-                          X.weights.ptr, b_ternary, b_n, b_k, m, n, k, k_blk, static_cast<int16_t*>(X.c.ptr), n,
-                          kernel, stream)))
-        return st;
-    LB_CUDA_TRY(cudaMemcpyAsync(c, X.c.ptr, (size_t)m * n * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
+    // A and C move in row chunks through a copy-in / compute / copy-out
+    // pipeline on three streams, so the PCIe directions overlap each other and
+    // the kernels (the host path is PCIe-bound: 2 B of C per output vs 1/4 B
+    // of A per input element).
+    if (!X.s_in) {
+        LB_CUDA_TRY(cudaStreamCreateWithFlags(&X.s_in, cudaStreamNonBlocking));
+        LB_CUDA_TRY(cudaStreamCreateWithFlags(&X.s_out, cudaStreamNonBlocking));
+        for (int i = 0; i < HostCtx::kChunks; ++i) {
+            LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_in[i], cudaEventDisableTiming));
+            LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_c[i], cudaEventDisableTiming));
+        }
+        LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_w, cudaEventDisableTiming));
+        LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_done, cudaEventDisableTiming));
+    }
+    const long long min_rows = 1024;  // keep per-chunk kernels large
+    int chunks = (int)((m + min_rows - 1) / min_rows);
+    if (chunks > HostCtx::kChunks) chunks = HostCtx::kChunks;
+    if (chunks < 1) chunks = 1;
+    // the copy streams must not run ahead of work already queued on `s`
+    LB_CUDA_TRY(cudaEventRecord(X.ev_w, s));
+    LB_CUDA_TRY(cudaStreamWaitEvent(X.s_in, X.ev_w, 0));
+    LB_CUDA_TRY(cudaStreamWaitEvent(X.s_out, X.ev_w, 0));
+    for (int ci = 0; ci < chunks; ++ci) {
+        const long long r0 = (long long)m * ci / chunks, r1 = (long long)m * (ci + 1) / chunks, rows = r1 - r0;
+        uint8_t* d0 = static_cast<uint8_t*>(X.a0.ptr) + r0 * pitch;
+        uint8_t* d1 = a_ternary ? static_cast<uint8_t*>(X.a1.ptr) + r0 * pitch : nullptr;
+        if (pitch == hstride) {
+            LB_CUDA_TRY(cudaMemcpyAsync(d0, a0 + r0 * hstride, rows * pitch, cudaMemcpyHostToDevice, X.s_in));
+            if (a_ternary)
+                LB_CUDA_TRY(cudaMemcpyAsync(d1, a1 + r0 * hstride, rows * pitch, cudaMemcpyHostToDevice, X.s_in));
+        } else {  // re-pitch to 16-byte rows; zero the padding first
+            LB_CUDA_TRY(cudaMemsetAsync(d0, 0, rows * pitch, X.s_in));
+            LB_CUDA_TRY(cudaMemcpy2DAsync(d0, pitch, a0 + r0 * hstride, hstride, hstride, rows,
+                                          cudaMemcpyHostToDevice, X.s_in));
+            if (a_ternary) {
+                LB_CUDA_TRY(cudaMemsetAsync(d1, 0, rows * pitch, X.s_in));
+                LB_CUDA_TRY(cudaMemcpy2DAsync(d1, pitch, a1 + r0 * hstride, hstride, hstride, rows,
+                                              cudaMemcpyHostToDevice, X.s_in));
+            }
+        }
+        LB_CUDA_TRY(cudaEventRecord(X.ev_in[ci], X.s_in));
+        LB_CUDA_TRY(cudaStreamWaitEvent(s, X.ev_in[ci], 0));
+        int16_t* dc = static_cast<int16_t*>(X.c.ptr) + r0 * n;
+        if ((st = lowbit_gemm(mode, d0, d1, pitch, (int)rows, a_cols, X.weights.ptr, b_ternary, b_n, b_k, (int)rows,
+                              n, k, k_blk, dc, n, kernel, stream)))
+            return st;
+        LB_CUDA_TRY(cudaEventRecord(X.ev_c[ci], s));
+        LB_CUDA_TRY(cudaStreamWaitEvent(X.s_out, X.ev_c[ci], 0));
+        LB_CUDA_TRY(cudaMemcpyAsync(c + r0 * n, dc, (size_t)rows * n * sizeof(int16_t), cudaMemcpyDeviceToHost,
+                                    X.s_out));
+    }
+    LB_CUDA_TRY(cudaEventRecord(X.ev_done, X.s_out));
+    LB_CUDA_TRY(cudaStreamWaitEvent(s, X.ev_done, 0));
     LB_CUDA_TRY(cudaStreamSynchronize(s));
     return LOWBIT_OK;
 }
