@@ -251,6 +251,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-config side measurements")
+    ap.add_argument("--no-gather", action="store_true", help="N>1: skip the (untimed) NCCL gather of C to rank 0")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -374,6 +375,24 @@ def main():
         del h_a0, h_a1, h_c
         ap_ref = None
 
+    gather = None
+    if world > 1 and not args.no_gather:
+        # NCCL output gather to rank 0 (only where a consumer needs the whole C;
+        # not part of `value`): int16 shards travel as bytes
+        from paper_2205_09120_b200.shard import gather_rows
+        dist.barrier()
+        torch.cuda.synchronize()
+        gs, ge = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gs.record()
+        full = gather_rows(c, M)
+        ge.record()
+        torch.cuda.synchronize()
+        tg = torch.tensor([gs.elapsed_time(ge)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        moved = (M - (r1 - r0)) * N * 2
+        gather = {"ms": tg.item(), "bytes_into_rank0": moved, "GB/s": moved / (tg.item() * 1e-3) / 1e9,
+                  "collective": "torch.distributed.gather (NCCL) of int16 shards as bytes"}
+        del full
     pk = peaks()
     tensor_peak = 2.0 * pk["bf16_tflops"]  # dense int8 tcgen05 = 2x bf16 per SM-clock (4.5 vs 2.25 PF spec)
     achieved = ops_rank / (kernel_ms_avg * 1e-3) / 1e12
@@ -415,7 +434,7 @@ def main():
                        "a_layout": "lanes (B200 lane-interleaved bit planes from K1)" if layout else "reference",
                        "parallelism": f"row-shard x{world}"},
             "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
-            "e2e": e2e, "per_config": extra,
+            "e2e": e2e, "gather": gather, "per_config": extra,
         }
         print(json.dumps(line))
     if world > 1:
@@ -468,13 +487,15 @@ def side_configs(lb, torch, flush, pk):
     for name in ("c1", "c3"):
         mode, M, N, K, da, db, seed = CONFIGS[name]
         a = lb.generate(da, seed, 0, M, K)
-        ap_ = lb.encode_binary(a) if mode == 0 else lb.encode_ternary(a)
+        # tensor kernels read the B200 lane-interleaved planes, the bit-serial kernel the reference ones
+        planes = {kid: (lb.encode_binary(a, layout=lay) if mode == 0 else lb.encode_ternary(a, layout=lay))
+                  for kid, lay in ((lb.KERNEL_TENSOR, 1), (lb.KERNEL_BITSERIAL, 0))}
         b = lb.generate(db, seed, 1, K, N)
         w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)))
         c = torch.empty((M, N), dtype=torch.int16, device="cuda")
         res = {}
         for kn, kid in kernels:
-            f = lambda: lb.gemm_lowbit(mode, ap_, w, (M, N, K), kernel=kid, out=c)
+            f = lambda: lb.gemm_lowbit(mode, planes[kid], w, (M, N, K), kernel=kid, out=c)
             ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
             tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
             res[kn] = {"ms": ms, "TOPS": tops,
@@ -546,13 +567,14 @@ def side_configs(lb, torch, flush, pk):
     del c5, w5
     # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
     planes = lb.empty_planes(1048576, 2048, True)
-    enc = lambda: L.check(L.lib.lowbit_encode(1, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,
-                                              C.c_void_p(planes.plane0.data_ptr()),
-                                              C.c_void_p(planes.plane1.data_ptr()), planes.pitch, None, st))
-    ms = time_device(torch, enc, flush, reps=5)
     eb = 1048576 * 2048 + 2 * 1048576 * planes.pitch
-    out["k1_encode_c5"] = {"ms": ms, "GB/s": eb / (ms * 1e-3) / 1e9, "frac_hbm": eb / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-                           "algorithmic_bytes": eb}
+    for lay, name in ((1, "k1_encode_c5_lanes"), (0, "k1_encode_c5_reference_layout")):
+        enc = lambda: L.check(L.lib.lowbit_encode_ex(1, lay, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,
+                                                     C.c_void_p(planes.plane0.data_ptr()),
+                                                     C.c_void_p(planes.plane1.data_ptr()), planes.pitch, None, st))
+        ms = time_device(torch, enc, flush, reps=5)
+        out[name] = {"ms": ms, "GB/s": eb / (ms * 1e-3) / 1e9, "frac_hbm": eb / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                     "algorithmic_bytes": eb}
     return out
 
 

@@ -285,7 +285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 #pragma unroll
                 for (int ch = 0; ch < 8; ++ch) sts_v4(row + (ch << 4), ch, ch, ch, ch);
             }
-            fence_proxy_async_smem();
+            if (!(prm.debug & 16)) fence_proxy_async_smem();  // debug 16: timing experiment without the fence
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&raw_empty[rs]);
