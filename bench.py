@@ -245,7 +245,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "bitserial"])
-    ap.add_argument("--layout", default="lanes", choices=["lanes", "reference"],
+    ap.add_argument("--layout", default="lanes", choices=["nibbles", "lanes", "reference"],
                     help="A plane layout written by the (untimed) encode: the B200 lane-interleaved layout or "
                          "the reference bit order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -280,7 +280,7 @@ def main():
 
     # ---- untimed setup: inputs in HBM, weights prepared ----
     a = lb.generate(da, seed, 0, m, K, row0=r0)
-    layout = 1 if (args.layout == "lanes" and args.kernel != "bitserial") else 0
+    layout = {"reference": 0, "lanes": 1, "nibbles": 2}[args.layout] if args.kernel != "bitserial" else 0
     ap_ = lb.encode_binary(a, layout=layout) if mode == 0 else lb.encode_ternary(a, layout=layout)
     ap_ref = None
     if not args.no_e2e and layout != 0:  # the host drop-in exchanges reference-layout planes

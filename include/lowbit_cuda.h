@@ -78,7 +78,15 @@ typedef void* lowbit_stream; /* cudaStream_t */
  *            8*(j%4) + j/4, so the tensor-core kernel turns a word into int8
  *            with one shift + mask per 4 elements.  A per-word bit
  *            permutation: popcounts, pitch and padding rules are unchanged. */
-typedef enum lowbit_layout { LOWBIT_LAYOUT_REFERENCE = 0, LOWBIT_LAYOUT_LANES = 1 } lowbit_layout;
+/* NIBBLES:  element j of each 32-bit word at bit 4*(j%8) + j/8, so
+ *            (w >> q) & 0x11111111 holds elements 8q..8q+7 one per nibble: the
+ *            fp4 (e2m1, kind::mxf4) tensor-core path builds its packed operand
+ *            with one shift + mask + multiply-add per 8 elements. */
+typedef enum lowbit_layout {
+    LOWBIT_LAYOUT_REFERENCE = 0,
+    LOWBIT_LAYOUT_LANES = 1,
+    LOWBIT_LAYOUT_NIBBLES = 2
+} lowbit_layout;
 
 /* ---- library / errors --------------------------------------------------- */
 int lowbit_abi_version(void);

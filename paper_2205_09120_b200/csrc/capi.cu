@@ -16,6 +16,9 @@ lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, c
                                  cudaStream_t stream);
 lowbit_status launch_tensor_pair_i8(const int8_t* a, long long lda, int m, int n, int k, const void* weights,
                                     int b_ternary, int16_t* c, long long ldc, cudaStream_t stream);
+lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+                              int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                              cudaStream_t stream);
 lowbit_status launch_tensor(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                             int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                             cudaStream_t stream);
@@ -153,7 +156,7 @@ extern "C" lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a
     if ((reinterpret_cast<uintptr_t>(weights) & 255))
         return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: weights must be 256-byte aligned");
     if (ldc < n) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: ldc < n");
-    if (a_layout != LOWBIT_LAYOUT_REFERENCE && a_layout != LOWBIT_LAYOUT_LANES)
+    if (a_layout != LOWBIT_LAYOUT_REFERENCE && a_layout != LOWBIT_LAYOUT_LANES && a_layout != LOWBIT_LAYOUT_NIBBLES)
         return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown A plane layout");
     if (kernel == LOWBIT_KERNEL_AUTO) kernel = lowbit_select_kernel(mode, m, n, k);
     cudaStream_t s = (cudaStream_t)stream;
@@ -161,6 +164,11 @@ extern "C" lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a
         if (a_layout != LOWBIT_LAYOUT_REFERENCE)
             return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: the bit-serial kernel reads REFERENCE-layout planes");
         return lb::launch_bitserial(mode, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    }
+    if (a_layout == LOWBIT_LAYOUT_NIBBLES) {  // fp4 tensor cores (CTA pairs for every m)
+        if (kernel != LOWBIT_KERNEL_TENSOR)
+            return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: NIBBLES planes run on the tensor-core pair kernel only");
+        return lb::launch_fp4_pair(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     }
     if (kernel == LOWBIT_KERNEL_TENSOR && m > 128)
         return lb::launch_tensor_pair(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);

@@ -147,6 +147,24 @@ LB_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
 }
 LB_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 32 lanes x 16 consecutive 32-bit columns.
+LB_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+// Store one value into 16 consecutive columns of this thread's TMEM lane.
+LB_DEV void tmem_st_32x32b_x16_fill(uint32_t taddr, uint32_t x) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(x)
+        : "memory");
+}
+LB_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, K-major operand, 128-byte swizzle:
 // rows of 128 bytes, 8-row swizzle atoms stacked every 1024 bytes (SBO),
@@ -260,6 +278,28 @@ LB_DEV void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Block-scaled fp4 pair MMA: D[tmem, f32] (+)= (A * SFA) x (B * SFB)^T with
+// packed e2m1 operands in shared memory (K = 64 per instruction) and one
+// UE8M0 scale per 32 depth positions read from TMEM.
+LB_DEV void umma_mxf4_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t tmem_sfa,
+                           uint32_t tmem_sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
+        : "memory");
+}
+// Instruction descriptor, block-scaled kind::mxf4: E2M1 A/B (format 1),
+// UE8M0 scales (bit 23), K-major, dense K = 64, scale-factor ids 0.
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t m, uint32_t n) {
+    return (1u << 7)            // a_format = E2M1
+           | (1u << 10)         // b_format = E2M1
+           | ((n >> 3) << 17)   // N
+           | (1u << 23)         // scale format UE8M0
+           | ((m >> 4) << 24);  // M
+}
+
 // Commit the pair's MMAs to the mbarrier at this offset in every CTA of cta_mask.
 LB_DEV void umma_commit_pair(uint64_t* bar, uint16_t cta_mask) {
     asm volatile(

@@ -33,9 +33,12 @@ __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, in
             if (LAYOUT == 0) {
                 encode_word32(values + r * ld + c0, nvals, plus, minus);
                 if (!ternary && ((plus | minus) != valid_mask32(nvals))) saw_zero = true;
-            } else {
+            } else if (LAYOUT == 1) {
                 encode_word32_lanes(values + r * ld + c0, nvals, plus, minus);
                 if (!ternary && ((plus | minus) != valid_mask32_lanes(nvals))) saw_zero = true;
+            } else {
+                encode_word32_nibbles(values + r * ld + c0, nvals, plus, minus);
+                if (!ternary && ((plus | minus) != valid_mask32_nibbles(nvals))) saw_zero = true;
             }
         }
         uint32_t* d0 = reinterpret_cast<uint32_t*>(plane0 + r * pitch);
@@ -181,6 +184,46 @@ __global__ void prepare_i8_kernel(int ternary, const uint8_t* __restrict__ panel
     }
 }
 
+// fp4 (e2m1) section: one thread per (column, 16-byte chunk = 32 depth
+// positions); +1 -> 0x2, -1 -> 0xA, 0 -> 0x0, element 2i in the low nibble
+// of byte i; zero past k.
+__global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ panels, int n, int k, int np, int kp4,
+                                   uint8_t* __restrict__ out) {
+    const int db = (k + 7) / 8;
+    const int chunks = kp4 / 32;
+    const long long total = (long long)np * chunks;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int col = (int)(idx / chunks);
+        const int ch = (int)(idx - (long long)col * chunks);
+        uint32_t words[4] = {0, 0, 0, 0};
+        if (col < n) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // 8 depth positions (one panel byte) per output word
+                const int d = ch * 4 + q;
+                if (d >= db) break;
+                uint32_t p, m;
+                if (ternary) {
+                    p = panel_byte(panels, 1, db, col, d, 0);
+                    m = panel_byte(panels, 1, db, col, d, 1);
+                } else {
+                    m = panel_byte(panels, 0, db, col, d, 0);
+                    const int valid = k - d * 8 < 8 ? k - d * 8 : 8;
+                    p = ~m & ((1u << valid) - 1u);
+                }
+                uint32_t w = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t code = ((p >> j) & 1u) ? 0x2u : (((m >> j) & 1u) ? 0xAu : 0x0u);
+                    w |= code << (4 * j);
+                }
+                words[q] = w;
+            }
+        }
+        reinterpret_cast<uint4*>(out + (size_t)col * (kp4 / 2))[ch] = make_uint4(words[0], words[1], words[2], words[3]);
+    }
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -220,7 +263,7 @@ extern "C" lowbit_status lowbit_encode(int ternary, const int8_t* values, int ro
 extern "C" lowbit_status lowbit_encode_ex(int ternary, int layout, const int8_t* values, int rows, int cols,
                                           long long ld, uint8_t* plane0, uint8_t* plane1, long long pitch,
                                           int* zero_flag, lowbit_stream stream) {
-    if (layout != LOWBIT_LAYOUT_REFERENCE && layout != LOWBIT_LAYOUT_LANES)
+    if (layout != LOWBIT_LAYOUT_REFERENCE && layout != LOWBIT_LAYOUT_LANES && layout != LOWBIT_LAYOUT_NIBBLES)
         return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "encode: unknown plane layout");
     if (rows < 0 || cols < 0) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "encode: negative shape");
     if (rows == 0 || cols == 0) return LOWBIT_OK;
@@ -233,8 +276,11 @@ extern "C" lowbit_status lowbit_encode_ex(int ternary, int layout, const int8_t*
     if (layout == LOWBIT_LAYOUT_REFERENCE)
         encode_kernel<0><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ternary, values, rows, cols, ld,
                                                                                  plane0, plane1, pitch, zero_flag);
-    else
+    else if (layout == LOWBIT_LAYOUT_LANES)
         encode_kernel<1><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ternary, values, rows, cols, ld,
+                                                                                 plane0, plane1, pitch, zero_flag);
+    else
+        encode_kernel<2><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ternary, values, rows, cols, ld,
                                                                                  plane0, plane1, pitch, zero_flag);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
@@ -274,6 +320,9 @@ extern "C" lowbit_status lowbit_prepare_weights(int ternary, const uint8_t* pane
     cudaStream_t s = (cudaStream_t)stream;
     prepare_i8_kernel<<<grid_for((long long)L.np * (L.kp / 16), 256), 256, 0, s>>>(
         ternary, panels, n, k, L.np, L.kp, reinterpret_cast<int8_t*>(base));
+    LB_CUDA_TRY(cudaGetLastError());
+    prepare_fp4_kernel<<<grid_for((long long)L.np * (L.kp4 / 32), 256), 256, 0, s>>>(
+        ternary, panels, n, k, L.np, L.kp4, base + L.off_fp4);
     LB_CUDA_TRY(cudaGetLastError());
     prepare_bits_kernel<<<grid_for((long long)L.np * L.kw, 256), 256, 0, s>>>(
         ternary, panels, n, k, L.np, L.kw, reinterpret_cast<uint32_t*>(base + L.off_sign),

@@ -65,6 +65,55 @@ __device__ __forceinline__ void encode_word32_lanes(const int8_t* src, int nvals
     }
 }
 
+// Same for the nibble-interleaved layout (LOWBIT_LAYOUT_NIBBLES): element j at
+// bit 4*(j%8) + j/8, so (w >> q) & 0x11111111 holds elements 8q..8q+7, one per
+// nibble — the packed-e2m1 order of the fp4 tensor-core path.  Built from the
+// per-byte flags of 4-value lane words: pairs (2t, 2t+1) interleave by
+// nibble at bit t, then one perfect unshuffle of the 8 nibbles.
+__device__ __forceinline__ uint32_t unshuffle_nibbles(uint32_t x) {
+    uint32_t t = (x ^ (x >> 4)) & 0x00F000F0u;
+    x = x ^ t ^ (t << 4);
+    t = (x ^ (x >> 8)) & 0x0000FF00u;
+    return x ^ t ^ (t << 8);
+}
+
+__device__ __forceinline__ void encode_word32_nibbles(const int8_t* src, int nvals, uint32_t& plus,
+                                                      uint32_t& minus) {
+    uint32_t v[8];
+    if (nvals == 32 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
+        const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+        v[0] = lo.x, v[1] = lo.y, v[2] = lo.z, v[3] = lo.w, v[4] = hi.x, v[5] = hi.y, v[6] = hi.z, v[7] = hi.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = 4 * i + b;
+                if (j < nvals) x |= (uint32_t)(uint8_t)src[j] << (8 * b);
+            }
+            v[i] = x;
+        }
+    }
+    uint32_t pa = 0, ma = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t ne = (v[2 * t] >> 7) & 0x01010101u, no = (v[2 * t + 1] >> 7) & 0x01010101u;
+        const uint32_t ze = nonzero_msb(v[2 * t]) >> 7, zo = nonzero_msb(v[2 * t + 1]) >> 7;
+        ma |= (ne | (no << 4)) << t;
+        pa |= ((ze & ~ne) | ((zo & ~no) << 4)) << t;
+    }
+    plus = unshuffle_nibbles(pa);
+    minus = unshuffle_nibbles(ma);
+}
+
+__device__ __forceinline__ uint32_t valid_mask32_nibbles(int nvals) {
+    uint32_t m = 0;
+    for (int j = 0; j < nvals && j < 32; ++j) m |= 1u << (4 * (j & 7) + (j >> 3));
+    return m;
+}
+
 // Bit mask of the first nvals elements in the lane-interleaved layout.
 __device__ __forceinline__ uint32_t valid_mask32_lanes(int nvals) {
     uint32_t m = 0;

@@ -1,0 +1,378 @@
+// gemm_fp4_pair.cu — K5: the bit-plane GeMM on the fp4 tensor cores.
+//
+// Same contract as K3 (gemm_tc_pair.cu) — ternary/binary A bit planes times
+// prepared weights, int16 out, bit-identical to gemm_lowbit (gemm.cpp:79-112)
+// — but the operands reach the tensor cores as packed e2m1 (4 bits/element)
+// through tcgen05.mma.cta_group::2.kind::mxf4.block_scale with every UE8M0
+// block scale = 1.0:
+//
+//   * {-1, 0, +1} are exact e2m1 codes (0xA, 0x0, 0x2); every partial sum is
+//     an integer of magnitude <= k <= 32767 < 2^24, so the f32 accumulator is
+//     exact and the epilogue's round-to-nearest is the identity.
+//   * an fp4 MMA does twice the int8 MMA's work per cycle on half the operand
+//     bytes, and A arrives in the NIBBLES plane layout (lowbit_encode_ex,
+//     layout 2: element j of a word at bit 4*(j%8) + j/8), so building a word
+//     of 8 packed e2m1 values costs one shift + mask per plane and an IMAD:
+//         ternary: ((M >> q) & 0x11111111) * 10 + ((P >> (q-1)) & 0x22222222)
+//         binary:  ((S >> q) & 0x11111111) * 8 + 0x22222222
+//     about 0.6 integer ops per element against 1.25 for the int8 lanes path.
+//
+// Tiling: a CTA pair computes 256 x BN (BN <= 224, multiple of 16; two f32
+// accumulators of BN columns + the scale-factor columns fit the 512 TMEM
+// columns), k-block = 256 depth positions = 128 bytes per row (one SW128
+// atom row).  Warp roles as K3: 0-7 converters (two groups of 4, alternate
+// k-blocks, one A row per thread), 8-11 epilogue, 12 raw-plane TMA producer,
+// 13 B TMA producer, 14 TMEM allocation + UMMA issue (leader CTA).
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "layout.cuh"
+#include "tmap.cuh"
+
+namespace lb {
+
+constexpr int F4_BM = 128;           // A rows per CTA (256 per pair)
+constexpr int F4_BK = 256;           // depth per k-block (128 bytes of packed e2m1)
+constexpr int F4_MAX_BN = 224;       // pair UMMA N (f32 accumulator columns per buffer)
+constexpr int F4_STAGES = 5;         // shared A/B ring
+constexpr int F4_RAW_STAGES = 6;     // raw bit-plane ring
+constexpr int F4_THREADS = 480;
+constexpr int F4_W_RAW = 12, F4_W_B = 13, F4_W_MMA = 14;
+constexpr int F4_A_BYTES = F4_BM * 128;       // 16 KB
+constexpr int F4_B_BYTES = 128 * 128;         // 16 KB slot (this CTA's <= 112 rows of B)
+constexpr int F4_RAW_PLANE = F4_BM * 32;      // 4 KB: 128 rows x 256 bits
+constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp per buffer
+constexpr uint32_t F4_SF_COL = 448;           // scale factors: SFA at 448, SFB at 480
+constexpr int F4_SMEM = 1024 + F4_STAGES * (F4_A_BYTES + F4_B_BYTES) + F4_RAW_STAGES * 2 * F4_RAW_PLANE +
+                        4 * 2 * F4_EPI_BYTES + 1024;
+static_assert(F4_SMEM <= 227 * 1024, "fp4 pair kernel exceeds shared memory");
+
+struct Fp4Params {
+    int m, n, kblocks, bn, m_tiles, n_tiles;
+    long long ldc;
+    int16_t* c;
+    int tma_store;
+};
+
+// One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1.
+template <bool A_TER>
+__device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) {
+    uint32_t o[4];
+    if (A_TER) {
+        o[0] = (m & 0x11111111u) * 10u + ((p << 1) & 0x22222222u);
+        o[1] = ((m >> 1) & 0x11111111u) * 10u + (p & 0x22222222u);
+        o[2] = ((m >> 2) & 0x11111111u) * 10u + ((p >> 1) & 0x22222222u);
+        o[3] = ((m >> 3) & 0x11111111u) * 10u + ((p >> 2) & 0x22222222u);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = ((p >> q) & 0x11111111u) * 8u + 0x22222222u;
+    }
+    sts_v4(dst, o[0], o[1], o[2], o[3]);
+}
+
+template <bool A_TER>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
+    gemm_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
+                         const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_c,
+                         const Fp4Params prm) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + F4_STAGES * F4_A_BYTES;
+    uint8_t* sRaw = sB + F4_STAGES * F4_B_BYTES;
+    uint8_t* sEpi = sRaw + F4_RAW_STAGES * 2 * F4_RAW_PLANE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * 2 * F4_EPI_BYTES);
+    uint64_t* raw_full = bars;                       // local: raw planes landed            [raw]
+    uint64_t* raw_empty = bars + 8;                  // local: 4 converter warps read them  [raw]
+    uint64_t* b_full = bars + 16;                    // leader: both halves of B landed     [ab]
+    uint64_t* a_ready = bars + 24;                   // leader: 8 converter warps done      [ab]
+    uint64_t* ab_empty = bars + 32;                  // local: pair MMAs done with the slot [ab]
+    uint64_t* tmem_full = bars + 40;                 // local: accumulator ready (2)
+    uint64_t* tmem_empty = bars + 42;                // leader: 8 epilogue warps drained (2)
+    uint64_t* sf_ready = bars + 44;                  // leader: scale factors written (8 warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 45);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int num_tiles = prm.m_tiles * prm.n_tiles;
+    const int bn = prm.bn, bnh = prm.bn >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < F4_RAW_STAGES; ++s) {
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&raw_empty[s], 4);
+        }
+        for (int s = 0; s < F4_STAGES; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&a_ready[s], 8);
+            mbar_init(&ab_empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 8);
+        }
+        mbar_init(sf_ready, 8);
+        fence_barrier_init();
+    }
+    if (warp == F4_W_RAW && lane == 0) {
+        tma_prefetch_desc(&tmap_b);
+        tma_prefetch_desc(&tmap_a0);
+        if (A_TER) tma_prefetch_desc(&tmap_a1);
+        if (prm.tma_store) tma_prefetch_desc(&tmap_c);
+    }
+    if (warp == F4_W_MMA) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == F4_W_RAW) {
+        // ===================== raw A-plane producer (both CTAs) =====================
+        if (lane == 0) {
+            const uint32_t raw_bytes = (A_TER ? 2 : 1) * F4_RAW_PLANE;
+            uint32_t t = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                const int mt = tile / prm.n_tiles;
+                const int arow = mt * 2 * F4_BM + (int)rank * F4_BM;
+                for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
+                    const uint32_t rs = t % F4_RAW_STAGES;
+                    mbar_wait_sleep(&raw_empty[rs], ((t / F4_RAW_STAGES) & 1) ^ 1);
+                    uint8_t* raw = sRaw + rs * 2 * F4_RAW_PLANE;
+                    mbar_arrive_expect_tx(&raw_full[rs], raw_bytes);
+                    tma_load_2d(raw, &tmap_a0, &raw_full[rs], kb * 32, arow);
+                    if (A_TER) tma_load_2d(raw + F4_RAW_PLANE, &tmap_a1, &raw_full[rs], kb * 32, arow);
+                }
+            }
+        }
+    } else if (warp == F4_W_B) {
+        // ===================== B producer (both CTAs; bytes land on the leader) =====================
+        if (lane == 0) {
+            const uint32_t pair_bytes = (uint32_t)bn * 128;
+            const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
+            uint32_t t = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
+                const int brow = nt * bn + (int)rank * bnh;
+                for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
+                    const uint32_t st = t % F4_STAGES;
+                    mbar_wait_sleep(&ab_empty[st], ((t / F4_STAGES) & 1) ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
+                    tma_load_2d_pair(smem_u32(sB + st * F4_B_BYTES), &tmap_b, b_full0 + st * 8, kb * 128, brow);
+                }
+            }
+        }
+    } else if (warp == F4_W_MMA) {
+        // ===================== UMMA issuer (leader CTA only) =====================
+        if (leader) {
+            const uint32_t idesc = idesc_mxf4(2 * F4_BM, (uint32_t)bn);
+            const uint32_t sfa = tmem_base + F4_SF_COL, sfb = tmem_base + F4_SF_COL + 32;
+            mbar_wait(sf_ready, 0);
+            tc_fence_after();
+            uint32_t t = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
+                for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
+                    const uint32_t st = t % F4_STAGES;
+                    mbar_wait(&a_ready[st], (t / F4_STAGES) & 1);
+                    mbar_wait(&b_full[st], (t / F4_STAGES) & 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a_addr = smem_u32(sA + st * F4_A_BYTES);
+                        const uint32_t b_addr = smem_u32(sB + st * F4_B_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)  // K = 64 per MMA = 32 bytes
+                            umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
+                                           umma_desc_k_sw128(b_addr + kk * 32), idesc, sfa, sfb, (kb | kk) != 0);
+                        umma_commit_pair(&ab_empty[st], 0x3);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) umma_commit_pair(&tmem_full[acc], 0x3);
+                __syncwarp();
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp < 8) {
+        // ===================== converters (both CTAs) =====================
+        const int g = warp >> 2;
+        const int r = threadIdx.x & 127;
+        const uint32_t sA_u = smem_u32(sA), sRaw_u = smem_u32(sRaw);
+        const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), 0);
+        const uint32_t total = (uint32_t)((num_tiles - pair + npairs - 1) / npairs) * (uint32_t)prm.kblocks;
+        const uint32_t rsw = (uint32_t)(r >> 2) & 1;  // TMA SWIZZLE_32B on the raw rows
+        for (uint32_t t = g; t < total; t += 2) {
+            const uint32_t rs = t % F4_RAW_STAGES, st = t % F4_STAGES;
+            mbar_wait_sleep(&raw_full[rs], (t / F4_RAW_STAGES) & 1);
+            mbar_wait_sleep(&ab_empty[st], ((t / F4_STAGES) & 1) ^ 1);
+            const uint32_t raw = sRaw_u + rs * 2 * F4_RAW_PLANE + r * 32;
+            const uint4 p0 = lds_v4(raw + (rsw << 4)), p1 = lds_v4(raw + ((rsw ^ 1) << 4));
+            uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0;
+            if (A_TER) {
+                m0 = lds_v4(raw + F4_RAW_PLANE + (rsw << 4));
+                m1 = lds_v4(raw + F4_RAW_PLANE + ((rsw ^ 1) << 4));
+            }
+            const uint32_t row = sA_u + st * F4_A_BYTES + r * 128;
+            const uint32_t sw = (uint32_t)r & 7;  // SW128: chunk c at c ^ (row % 8)
+            fp4_chunk<A_TER>(p0.x, m0.x, row + ((0 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.y, m0.y, row + ((1 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.z, m0.z, row + ((2 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.w, m0.w, row + ((3 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.x, m1.x, row + ((4 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&raw_empty[rs]);
+                mbar_arrive_cluster(a_ready0 + st * 8);
+            }
+        }
+    } else {
+        // ===================== epilogue (both CTAs) =====================
+        const int wq = warp & 3;  // TMEM lane quarter
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        // unit block scales (UE8M0 0x7F = 2^0) for both operands, then let the MMAs start
+#pragma unroll
+        for (uint32_t col = F4_SF_COL; col < 512; col += 16)
+            tmem_st_32x32b_x16_fill(tmem_base + lane_base + col, 0x7F7F7F7Fu);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(sf_ready), 0));
+
+        const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
+        const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * 2 * F4_EPI_BYTES;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int nbuf = 0;
+        for (int tile = pair; tile < num_tiles; tile += npairs) {
+            const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
+            const int row0 = mt * 2 * F4_BM + (int)rank * F4_BM + wq * 32;
+            mbar_wait_sleep(&tmem_full[acc], acc_phase);
+            tc_fence_after();
+            for (int ch = 0; ch < bn / 16; ++ch) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN + ch * 16, v);
+                tmem_ld_wait();
+                uint32_t h[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    h[j] = __byte_perm((uint32_t)__float2int_rn(__uint_as_float(v[2 * j])),
+                                       (uint32_t)__float2int_rn(__uint_as_float(v[2 * j + 1])), 0x5410);
+                const int col0 = nt * bn + ch * 16;
+                if (prm.tma_store) {
+                    const uint32_t buf = epi + (uint32_t)nbuf * F4_EPI_BYTES;
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                    const uint32_t rowaddr = buf + lane * 32;
+                    const uint32_t sw = (uint32_t)(lane >> 2) & 1;  // TMA SWIZZLE_32B
+                    sts_v4(rowaddr + (sw << 4), h[0], h[1], h[2], h[3]);
+                    sts_v4(rowaddr + ((sw ^ 1) << 4), h[4], h[5], h[6], h[7]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmap_c, buf, col0, row0);
+                        bulk_commit();
+                    }
+                    nbuf ^= 1;
+                } else {
+                    const int row = row0 + lane;
+                    if (row < prm.m) {
+                        int16_t* crow = prm.c + (long long)row * prm.ldc;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (col0 + j < prm.n) crow[col0 + j] = (int16_t)(h[j >> 1] >> (16 * (j & 1)));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (prm.tma_store && lane == 0) bulk_wait<0>();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == F4_W_MMA) {
+        tc_fence_after();
+        tmem_dealloc_pair<512>(tmem_base);
+    }
+}
+
+// BN: the fewest column tiles of <= 224, then the smallest multiple of 16 covering n.
+static int pick_bn_fp4(int n) {
+    const int tiles = (n + F4_MAX_BN - 1) / F4_MAX_BN;
+    const int per = (n + tiles - 1) / tiles;
+    return (per + 15) / 16 * 16;
+}
+
+template <bool A_TER>
+static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
+                                        const CUtensorMap& mc, const Fp4Params& prm, int pairs, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_pair_kernel<A_TER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         F4_SMEM));
+        attr = true;
+    }
+    gemm_fp4_pair_kernel<A_TER><<<2 * pairs, F4_THREADS, F4_SMEM, stream>>>(mb, ma0, ma1, mc, prm);
+    LB_CUDA_TRY(cudaGetLastError());
+    return LOWBIT_OK;
+}
+
+// A as NIBBLES-layout bit planes (lowbit_encode_ex layout 2).
+lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+                              int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
+                              cudaStream_t stream) {
+    const WeightsLayout L(b_ternary, n, k);
+    Fp4Params prm{};
+    prm.m = m;
+    prm.n = n;
+    prm.kblocks = L.kp4 / F4_BK;
+    prm.bn = pick_bn_fp4(n);
+    prm.m_tiles = (m + 2 * F4_BM - 1) / (2 * F4_BM);
+    prm.n_tiles = (n + prm.bn - 1) / prm.bn;
+    prm.ldc = ldc;
+    prm.c = c;
+    prm.tma_store = ((ldc * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    CUtensorMap mb, ma0, ma1, mc;
+    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
+    if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 128, (uint32_t)(prm.bn / 2),
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for fp4 B");
+    if (prm.tma_store) {
+        if (!make_map_2d(&mc, c, (uint64_t)n, (uint64_t)m, (uint64_t)ldc * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B,
+                         CU_TENSOR_MAP_DATA_TYPE_UINT16))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for C");
+    } else {
+        mc = mb;
+    }
+    if (!make_map_2d(&ma0, a0, (uint64_t)a_pitch, (uint64_t)m, (uint64_t)a_pitch, 32, F4_BM,
+                     CU_TENSOR_MAP_SWIZZLE_32B))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for A");
+    if (a_ternary) {
+        if (!make_map_2d(&ma1, a1, (uint64_t)a_pitch, (uint64_t)m, (uint64_t)a_pitch, 32, F4_BM,
+                         CU_TENSOR_MAP_SWIZZLE_32B))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for A minus");
+    } else {
+        ma1 = ma0;
+    }
+    const int tiles = prm.m_tiles * prm.n_tiles;
+    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    return a_ternary ? launch_fp4_variant<true>(mb, ma0, ma1, mc, prm, pairs, stream)
+                     : launch_fp4_variant<false>(mb, ma0, ma1, mc, prm, pairs, stream);
+}
+
+}  // namespace lb

@@ -8,6 +8,10 @@
 //                     element's minus bit (binary: its only bit).
 //   [ nz words     ]  ternary only: np x kw uint32, plus|minus bits.
 //                     Read by K2 (bit-serial).
+//   [ fp4 section  ]  np x kp4/2 bytes, K-major packed e2m1 (+1 = 0x2,
+//                     -1 = 0xA, 0 = 0x0; element 2i in the low nibble of
+//                     byte i), kp4 a multiple of 256: the UMMA B operand of
+//                     the kind::mxf4 path.
 #pragma once
 #include <cstddef>
 
@@ -18,15 +22,18 @@ struct WeightsLayout {
     int np;  // rows padded to a multiple of 256
     int kp;  // int8 row length, multiple of 128 bytes (one UMMA k-block)
     int kw;  // words per column in the bit sections, multiple of 8 (one K2 stage)
-    size_t off_sign, off_nz, bytes;
+    int kp4; // fp4 row length in elements, multiple of 256 (one 128-byte fp4 k-block)
+    size_t off_sign, off_nz, off_fp4, bytes;
 
     __host__ __device__ WeightsLayout(int ternary_, int n_, int k_) : ternary(ternary_), n(n_), k(k_) {
         np = (n + 255) / 256 * 256;
         kp = (k + 127) / 128 * 128;
         kw = ((k + 31) / 32 + 7) / 8 * 8;
+        kp4 = (k + 255) / 256 * 256;
         off_sign = (size_t)np * kp;
         off_nz = off_sign + (size_t)np * kw * 4;
-        bytes = off_nz + (ternary ? (size_t)np * kw * 4 : 0);
+        off_fp4 = (off_nz + (ternary ? (size_t)np * kw * 4 : 0) + 1023) / 1024 * 1024;
+        bytes = off_fp4 + (size_t)np * kp4 / 2;
     }
 };
 
