@@ -36,16 +36,20 @@ constexpr int F4_BM = 128;           // A rows per CTA (256 per pair)
 constexpr int F4_BK = 256;           // depth per k-block (128 bytes of packed e2m1)
 constexpr int F4_MAX_BN = 224;       // pair UMMA N (f32 accumulator columns per buffer)
 constexpr int F4_STAGES = 5;         // shared A/B ring
-constexpr int F4_RAW_STAGES = 6;     // raw bit-plane ring
 constexpr int F4_THREADS = 480;
 constexpr int F4_W_RAW = 12, F4_W_B = 13, F4_W_MMA = 14;
 constexpr int F4_A_BYTES = F4_BM * 128;       // 16 KB
-constexpr int F4_B_BYTES = 128 * 128;         // 16 KB slot (this CTA's <= 112 rows of B)
+constexpr int F4_B_BYTES = (F4_MAX_BN / 2) * 128;  // 14 KB slot (this CTA's <= 112 rows of B)
 constexpr int F4_RAW_PLANE = F4_BM * 32;      // 4 KB: 128 rows x 256 bits
+// Raw bit-plane ring: 64 KB = 8 ternary (two-plane) or 16 binary k-blocks.
+// When a CTA's whole depth fits (k <= 2048 ternary / 4096 binary), the ring
+// holds its A rows for all the column tiles of an m-tile: the planes cross
+// L2 -> SM once per m-tile instead of once per (m, n) tile.
+constexpr int F4_RAW_RING = 64 * 1024;
+__host__ __device__ constexpr int f4_raw_stages(bool ter) { return ter ? 8 : 16; }
 constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp per buffer
 constexpr uint32_t F4_SF_COL = 448;           // scale factors: SFA at 448, SFB at 480
-constexpr int F4_SMEM = 1024 + F4_STAGES * (F4_A_BYTES + F4_B_BYTES) + F4_RAW_STAGES * 2 * F4_RAW_PLANE +
-                        4 * 2 * F4_EPI_BYTES + 1024;
+constexpr int F4_SMEM = 1024 + F4_STAGES * (F4_A_BYTES + F4_B_BYTES) + F4_RAW_RING + 4 * 2 * F4_EPI_BYTES + 1024;
 static_assert(F4_SMEM <= 227 * 1024, "fp4 pair kernel exceeds shared memory");
 
 struct Fp4Params {
@@ -53,6 +57,9 @@ struct Fp4Params {
     long long ldc;
     int16_t* c;
     int tma_store;
+    int m_major;   // schedule: 1 = each pair owns whole m tiles (all n tiles back to back)
+    int resident;  // raw A planes stay in the ring across the n tiles of an m tile (m_major only)
+    int debug;  // timing experiments only (results invalid): 1 converters skip the expansion, 2 no MMAs
 };
 
 // One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1.
@@ -81,28 +88,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     uint8_t* sA = smem;
     uint8_t* sB = sA + F4_STAGES * F4_A_BYTES;
     uint8_t* sRaw = sB + F4_STAGES * F4_B_BYTES;
-    uint8_t* sEpi = sRaw + F4_RAW_STAGES * 2 * F4_RAW_PLANE;
+    uint8_t* sEpi = sRaw + F4_RAW_RING;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * 2 * F4_EPI_BYTES);
+    constexpr uint32_t RS = f4_raw_stages(A_TER);
+    constexpr uint32_t RAW_SLOT = A_TER ? 2 * F4_RAW_PLANE : F4_RAW_PLANE;
     uint64_t* raw_full = bars;                       // local: raw planes landed            [raw]
-    uint64_t* raw_empty = bars + 8;                  // local: 4 converter warps read them  [raw]
-    uint64_t* b_full = bars + 16;                    // leader: both halves of B landed     [ab]
-    uint64_t* a_ready = bars + 24;                   // leader: 8 converter warps done      [ab]
-    uint64_t* ab_empty = bars + 32;                  // local: pair MMAs done with the slot [ab]
-    uint64_t* tmem_full = bars + 40;                 // local: accumulator ready (2)
-    uint64_t* tmem_empty = bars + 42;                // leader: 8 epilogue warps drained (2)
-    uint64_t* sf_ready = bars + 44;                  // leader: scale factors written (8 warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 45);
+    uint64_t* raw_empty = bars + 16;                 // local: 4 converter warps read them  [raw]
+    uint64_t* b_full = bars + 32;                    // leader: both halves of B landed     [ab]
+    uint64_t* a_ready = bars + 40;                   // leader: 8 converter warps done      [ab]
+    uint64_t* ab_empty = bars + 48;                  // local: pair MMAs done with the slot [ab]
+    uint64_t* tmem_full = bars + 56;                 // local: accumulator ready (2)
+    uint64_t* tmem_empty = bars + 58;                // leader: 8 epilogue warps drained (2)
+    uint64_t* sf_ready = bars + 60;                  // leader: scale factors written (8 warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 61);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    // Schedule.  m_major: pair p owns m tiles p, p + npairs, ... and runs every
+    // n tile of one m tile back to back (so its A rows can stay resident);
+    // otherwise (fewer m tiles than pairs) tiles are dealt round-robin.
     const int num_tiles = prm.m_tiles * prm.n_tiles;
+    const int my_tiles = prm.m_major ? (prm.m_tiles > pair ? (prm.m_tiles - pair + npairs - 1) / npairs : 0) * prm.n_tiles
+                                     : (num_tiles > pair ? (num_tiles - pair + npairs - 1) / npairs : 0);
+    auto tile_of = [&](int i, int& mt, int& nt) {
+        if (prm.m_major) {
+            mt = pair + (i / prm.n_tiles) * npairs;
+            nt = i % prm.n_tiles;
+        } else {
+            const int tile = pair + i * npairs;
+            mt = tile / prm.n_tiles;
+            nt = tile - mt * prm.n_tiles;
+        }
+    };
     const int bn = prm.bn, bnh = prm.bn >> 1;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < F4_RAW_STAGES; ++s) {
+        for (int s = 0; s < (int)RS; ++s) {
             mbar_init(&raw_full[s], 1);
             mbar_init(&raw_empty[s], 4);
         }
@@ -133,16 +157,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     if (warp == F4_W_RAW) {
         // ===================== raw A-plane producer (both CTAs) =====================
         if (lane == 0) {
-            const uint32_t raw_bytes = (A_TER ? 2 : 1) * F4_RAW_PLANE;
-            uint32_t t = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int mt = tile / prm.n_tiles;
+            uint32_t u = 0;  // raw loads issued
+            for (int i = 0; i < my_tiles; ++i) {
+                int mt, nt;
+                tile_of(i, mt, nt);
+                if (prm.resident && nt != 0) continue;
                 const int arow = mt * 2 * F4_BM + (int)rank * F4_BM;
-                for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
-                    const uint32_t rs = t % F4_RAW_STAGES;
-                    mbar_wait_sleep(&raw_empty[rs], ((t / F4_RAW_STAGES) & 1) ^ 1);
-                    uint8_t* raw = sRaw + rs * 2 * F4_RAW_PLANE;
-                    mbar_arrive_expect_tx(&raw_full[rs], raw_bytes);
+                for (int kb = 0; kb < prm.kblocks; ++kb, ++u) {
+                    const uint32_t rs = u % RS;
+                    mbar_wait_sleep(&raw_empty[rs], ((u / RS) & 1) ^ 1);
+                    uint8_t* raw = sRaw + rs * RAW_SLOT;
+                    mbar_arrive_expect_tx(&raw_full[rs], RAW_SLOT);
                     tma_load_2d(raw, &tmap_a0, &raw_full[rs], kb * 32, arow);
                     if (A_TER) tma_load_2d(raw + F4_RAW_PLANE, &tmap_a1, &raw_full[rs], kb * 32, arow);
                 }
@@ -154,8 +179,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             const uint32_t pair_bytes = (uint32_t)bn * 128;
             const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
             uint32_t t = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
+            for (int i = 0; i < my_tiles; ++i) {
+                int mt, nt;
+                tile_of(i, mt, nt);
                 const int brow = nt * bn + (int)rank * bnh;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t st = t % F4_STAGES;
@@ -175,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             uint32_t t = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs) {
+            for (int i = 0; i < my_tiles; ++i) {
                 mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
@@ -189,6 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         const uint32_t b_addr = smem_u32(sB + st * F4_B_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)  // K = 64 per MMA = 32 bytes
+                            if (!(prm.debug & 2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                            umma_desc_k_sw128(b_addr + kk * 32), idesc, sfa, sfb, (kb | kk) != 0);
                         umma_commit_pair(&ab_empty[st], 0x3);
@@ -206,13 +233,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         const int r = threadIdx.x & 127;
         const uint32_t sA_u = smem_u32(sA), sRaw_u = smem_u32(sRaw);
         const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), 0);
-        const uint32_t total = (uint32_t)((num_tiles - pair + npairs - 1) / npairs) * (uint32_t)prm.kblocks;
+        const uint32_t kbs = (uint32_t)prm.kblocks, nts = (uint32_t)prm.n_tiles;
+        const uint32_t total = (uint32_t)my_tiles * kbs;
         const uint32_t rsw = (uint32_t)(r >> 2) & 1;  // TMA SWIZZLE_32B on the raw rows
         for (uint32_t t = g; t < total; t += 2) {
-            const uint32_t rs = t % F4_RAW_STAGES, st = t % F4_STAGES;
-            mbar_wait_sleep(&raw_full[rs], (t / F4_RAW_STAGES) & 1);
+            // raw load index of this k-block: resident rings load once per m tile
+            const uint32_t seq = t / kbs, kb = t - seq * kbs;
+            const uint32_t nt = seq % nts;
+            const uint32_t u = prm.resident ? (seq / nts) * kbs + kb : t;
+            const bool release = !prm.resident || nt == nts - 1;
+            const uint32_t rs = u % RS, st = t % F4_STAGES;
+            mbar_wait_sleep(&raw_full[rs], (u / RS) & 1);
             mbar_wait_sleep(&ab_empty[st], ((t / F4_STAGES) & 1) ^ 1);
-            const uint32_t raw = sRaw_u + rs * 2 * F4_RAW_PLANE + r * 32;
+            const uint32_t raw = sRaw_u + rs * RAW_SLOT + r * 32;
+            if (prm.debug & 1) goto done;
+            {
             const uint4 p0 = lds_v4(raw + (rsw << 4)), p1 = lds_v4(raw + ((rsw ^ 1) << 4));
             uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0;
             if (A_TER) {
@@ -229,10 +264,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
             fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
             fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+            }
+        done:
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&raw_empty[rs]);
+                if (release) mbar_arrive(&raw_empty[rs]);
                 mbar_arrive_cluster(a_ready0 + st * 8);
             }
         }
@@ -254,20 +291,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int nbuf = 0;
-        for (int tile = pair; tile < num_tiles; tile += npairs) {
-            const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
+        for (int i = 0; i < my_tiles; ++i) {
+            int mt, nt;
+            tile_of(i, mt, nt);
             const int row0 = mt * 2 * F4_BM + (int)rank * F4_BM + wq * 32;
             mbar_wait_sleep(&tmem_full[acc], acc_phase);
             tc_fence_after();
-            for (int ch = 0; ch < bn / 16; ++ch) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN + ch * 16, v);
-                tmem_ld_wait();
+            // f32 -> int16 without F2I (quarter rate): x + 1.5 * 2^23 puts the
+            // integer x (|x| <= 32767) in the low mantissa bits, so its low
+            // half-word IS the int16 result.
+            auto emit = [&](const uint32_t (&v)[16], int ch) {
                 uint32_t h[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    h[j] = __byte_perm((uint32_t)__float2int_rn(__uint_as_float(v[2 * j])),
-                                       (uint32_t)__float2int_rn(__uint_as_float(v[2 * j + 1])), 0x5410);
+                    h[j] = __byte_perm(__float_as_uint(__uint_as_float(v[2 * j]) + 12582912.0f),
+                                       __float_as_uint(__uint_as_float(v[2 * j + 1]) + 12582912.0f), 0x5410);
                 const int col0 = nt * bn + ch * 16;
                 if (prm.tma_store) {
                     const uint32_t buf = epi + (uint32_t)nbuf * F4_EPI_BYTES;
@@ -293,6 +331,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                             if (col0 + j < prm.n) crow[col0 + j] = (int16_t)(h[j >> 1] >> (16 * (j & 1)));
                     }
                 }
+            };
+            const uint32_t tacc = tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN;
+            const int nch = (prm.debug & 4) ? 0 : bn / 16;
+            for (int ch = 0; ch < nch; ch += 2) {  // two TMEM loads in flight per wait
+                uint32_t va[16], vb[16];
+                tmem_ld_32x32b_x16(tacc + ch * 16, va);
+                if (ch + 1 < nch) tmem_ld_32x32b_x16(tacc + (ch + 1) * 16, vb);
+                tmem_ld_wait();
+                emit(va, ch);
+                if (ch + 1 < nch) emit(vb, ch + 1);
             }
             tc_fence_before();
             __syncwarp();
@@ -347,6 +395,17 @@ lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a
     prm.ldc = ldc;
     prm.c = c;
     prm.tma_store = ((ldc * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    // resident raw ring: the whole depth fits, and each k-block is always
+    // handled by the same converter group (even k-block count) so its last
+    // reader is the one that frees it
+    prm.m_major = prm.m_tiles >= num_sms() / 2;
+    prm.resident = prm.m_major && prm.kblocks <= f4_raw_stages(a_ternary != 0) &&
+                   (prm.kblocks % 2 == 0 || prm.n_tiles == 1);
+    static const int debug = [] {
+        const char* e = getenv("LOWBIT_DEBUG_FP4");
+        return e ? atoi(e) : 0;
+    }();
+    prm.debug = debug;
     CUtensorMap mb, ma0, ma1, mc;
     const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
     if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 128, (uint32_t)(prm.bn / 2),
@@ -369,8 +428,8 @@ lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a
     } else {
         ma1 = ma0;
     }
-    const int tiles = prm.m_tiles * prm.n_tiles;
-    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    const int work = prm.m_major ? prm.m_tiles : prm.m_tiles * prm.n_tiles;
+    const int pairs = work < num_sms() / 2 ? work : num_sms() / 2;
     return a_ternary ? launch_fp4_variant<true>(mb, ma0, ma1, mc, prm, pairs, stream)
                      : launch_fp4_variant<false>(mb, ma0, ma1, mc, prm, pairs, stream);
 }

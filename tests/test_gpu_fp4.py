@@ -90,6 +90,20 @@ def test_gemm_fp4_matches_oracle(lb, port, mode):
         assert (got == port.gemm(mode, a, b)).all(), (mode, m, n, k)
 
 
+# m >= 74 pair tiles (19k rows): the m-major schedule; k-block counts that keep
+# the raw planes resident (even, <= 8 ternary / 16 binary), odd ones, and
+# depths past the ring (streamed).
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+@pytest.mark.parametrize("k", [1000, 700, 2300, 4096])
+def test_gemm_fp4_m_major_schedule(lb, port, mode, k):
+    m, n = 19000, 300
+    da, db = mode_dists(mode)
+    a = port.generate(da, 300 + k, 0, m, k)
+    b = port.generate(db, 300 + k, 1, k, n)
+    got = host(lb.gemm_lowbit(mode, encode_a(lb, mode, a), weights(lb, mode, b), (m, n, k), kernel=2))
+    assert (got == port.gemm(mode, a, b)).all(), (mode, m, n, k)
+
+
 @pytest.mark.parametrize("mode", [BNN, TNN, TBN])
 def test_gemm_fp4_depth_extremes(lb, port, mode):
     """k = k_max = 32767: |C| reaches 32767, so the f32 accumulator must stay exact."""
