@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblowbit_cuda.so")
+# LOWBIT_LIB: alternative build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("LOWBIT_LIB") or os.path.join(HERE, "liblowbit_cuda.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "lowbit_cuda.h")
 
 # lowbit_status

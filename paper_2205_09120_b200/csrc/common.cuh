@@ -164,6 +164,10 @@ LB_DEV void tmem_st_32x32b_x16_fill(uint32_t taddr, uint32_t x) {
         "r"(x)
         : "memory");
 }
+LB_DEV void tmem_st_32x32b_x8_fill(uint32_t taddr, uint32_t x) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(x)
+                 : "memory");
+}
 LB_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, K-major operand, 128-byte swizzle:

@@ -34,21 +34,33 @@ namespace lb {
 
 constexpr int F4_BM = 128;           // A rows per CTA (256 per pair)
 constexpr int F4_BK = 256;           // depth per k-block (128 bytes of packed e2m1)
-constexpr int F4_MAX_BN = 224;       // pair UMMA N (f32 accumulator columns per buffer)
-constexpr int F4_STAGES = 5;         // shared A/B ring
+constexpr int F4_MAX_BN = 256;       // pair UMMA N (f32 accumulator columns per buffer)
+#ifndef LOWBIT_F4_STAGES
+#define LOWBIT_F4_STAGES 4
+#endif
+#ifndef LOWBIT_F4_RAW_KB
+#define LOWBIT_F4_RAW_KB 64
+#endif
+constexpr int F4_STAGES = LOWBIT_F4_STAGES;  // shared A/B ring
 constexpr int F4_THREADS = 480;
 constexpr int F4_W_RAW = 12, F4_W_B = 13, F4_W_MMA = 14;
 constexpr int F4_A_BYTES = F4_BM * 128;       // 16 KB
-constexpr int F4_B_BYTES = (F4_MAX_BN / 2) * 128;  // 14 KB slot (this CTA's <= 112 rows of B)
+constexpr int F4_B_BYTES = (F4_MAX_BN / 2) * 128;  // 16 KB slot (this CTA's <= 128 rows of B)
 constexpr int F4_RAW_PLANE = F4_BM * 32;      // 4 KB: 128 rows x 256 bits
 // Raw bit-plane ring: 64 KB = 8 ternary (two-plane) or 16 binary k-blocks.
 // When a CTA's whole depth fits (k <= 2048 ternary / 4096 binary), the ring
 // holds its A rows for all the column tiles of an m-tile: the planes cross
 // L2 -> SM once per m-tile instead of once per (m, n) tile.
-constexpr int F4_RAW_RING = 64 * 1024;
-__host__ __device__ constexpr int f4_raw_stages(bool ter) { return ter ? 8 : 16; }
+constexpr int F4_RAW_RING = LOWBIT_F4_RAW_KB * 1024;
+__host__ __device__ constexpr int f4_raw_stages(bool ter) { return LOWBIT_F4_RAW_KB / (ter ? 8 : 4); }
 constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp per buffer
-constexpr uint32_t F4_SF_COL = 448;           // scale factors: SFA at 448, SFB at 480
+// Scale factors.  An fp4 MMA costs the same for any N <= 256 (measured), so
+// tiles are 256 wide, and two f32 accumulators fill all 512 TMEM columns.
+// The unit scales (SFA and SFB share one 8-column block of 0x7F bytes) live
+// in the LAST 8 columns of the accumulator NOT being written: tile i
+// (buffer b) reads them from buffer 1-b's tail, which the epilogue of tile
+// i-1 drains first and then overwrites with scales (sf_ready[1-b]).
+constexpr uint32_t F4_SF_OFF = 248;
 constexpr int F4_SMEM = 1024 + F4_STAGES * (F4_A_BYTES + F4_B_BYTES) + F4_RAW_RING + 4 * 2 * F4_EPI_BYTES + 1024;
 static_assert(F4_SMEM <= 227 * 1024, "fp4 pair kernel exceeds shared memory");
 
@@ -92,6 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * 2 * F4_EPI_BYTES);
     constexpr uint32_t RS = f4_raw_stages(A_TER);
     constexpr uint32_t RAW_SLOT = A_TER ? 2 * F4_RAW_PLANE : F4_RAW_PLANE;
+    static_assert(RS <= 16 && F4_STAGES <= 8, "barrier table sizes");
     uint64_t* raw_full = bars;                       // local: raw planes landed            [raw]
     uint64_t* raw_empty = bars + 16;                 // local: 4 converter warps read them  [raw]
     uint64_t* b_full = bars + 32;                    // leader: both halves of B landed     [ab]
@@ -99,8 +112,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     uint64_t* ab_empty = bars + 48;                  // local: pair MMAs done with the slot [ab]
     uint64_t* tmem_full = bars + 56;                 // local: accumulator ready (2)
     uint64_t* tmem_empty = bars + 58;                // leader: 8 epilogue warps drained (2)
-    uint64_t* sf_ready = bars + 60;                  // leader: scale factors written (8 warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 61);
+    uint64_t* sf_ready = bars + 60;                  // leader: scales in buffer c's tail (8 warps) (2)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 62);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -139,7 +152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 8);
         }
-        mbar_init(sf_ready, 8);
+        mbar_init(&sf_ready[0], 8);
+        mbar_init(&sf_ready[1], 8);
         fence_barrier_init();
     }
     if (warp == F4_W_RAW && lane == 0) {
@@ -195,16 +209,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         // ===================== UMMA issuer (leader CTA only) =====================
         if (leader) {
             const uint32_t idesc = idesc_mxf4(2 * F4_BM, (uint32_t)bn);
-            const uint32_t sfa = tmem_base + F4_SF_COL, sfb = tmem_base + F4_SF_COL + 32;
-            mbar_wait(sf_ready, 0);
-            tc_fence_after();
             uint32_t t = 0;
             int acc = 0;
-            uint32_t acc_phase = 0;
+            uint32_t acc_phase = 0, sf_phase = 0;  // sf_phase bit c: parity of the next wait on sf_ready[c]
             for (int i = 0; i < my_tiles; ++i) {
                 mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
+                mbar_wait(&sf_ready[acc ^ 1], (sf_phase >> (acc ^ 1)) & 1);
+                sf_phase ^= 1u << (acc ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
+                const uint32_t sf = tmem_base + (uint32_t)(acc ^ 1) * F4_MAX_BN + F4_SF_OFF;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t st = t % F4_STAGES;
                     mbar_wait(&a_ready[st], (t / F4_STAGES) & 1);
@@ -217,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         for (int kk = 0; kk < 4; ++kk)  // K = 64 per MMA = 32 bytes
                             if (!(prm.debug & 2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
-                                           umma_desc_k_sw128(b_addr + kk * 32), idesc, sfa, sfb, (kb | kk) != 0);
+                                           umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf, (kb | kk) != 0);
                         umma_commit_pair(&ab_empty[st], 0x3);
                     }
                     __syncwarp();
@@ -277,14 +291,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         // ===================== epilogue (both CTAs) =====================
         const int wq = warp & 3;  // TMEM lane quarter
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        // unit block scales (UE8M0 0x7F = 2^0) for both operands, then let the MMAs start
-#pragma unroll
-        for (uint32_t col = F4_SF_COL; col < 512; col += 16)
-            tmem_st_32x32b_x16_fill(tmem_base + lane_base + col, 0x7F7F7F7Fu);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(sf_ready), 0));
+        const uint32_t sf_ready0 = mapa_shared(smem_u32(&sf_ready[0]), 0);
+        // unit block scales (UE8M0 0x7F = 2^0) into buffer c's tail, then tell the MMA warp
+        auto put_scales = [&](int c) {
+            tmem_st_32x32b_x8_fill(tmem_base + lane_base + (uint32_t)c * F4_MAX_BN + F4_SF_OFF, 0x7F7F7F7Fu);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(sf_ready0 + c * 8);
+        };
+        put_scales(1);  // tile 0 runs on buffer 0
 
         const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
         const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * 2 * F4_EPI_BYTES;
@@ -297,6 +313,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             const int row0 = mt * 2 * F4_BM + (int)rank * F4_BM + wq * 32;
             mbar_wait_sleep(&tmem_full[acc], acc_phase);
             tc_fence_after();
+            const uint32_t tacc = tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN;
+            const int nch = (prm.debug & 4) ? 0 : bn / 16;
+            // tail first: the next tile's scales go there (its last chunk waits in registers)
+            uint32_t vt[16];
+            const bool tail_out = bn > (int)F4_SF_OFF && nch > 0;
+            if (tail_out) {
+                tmem_ld_32x32b_x16(tacc + (nch - 1) * 16, vt);
+                tmem_ld_wait();
+            }
+            put_scales(acc);
             // f32 -> int16 without F2I (quarter rate): x + 1.5 * 2^23 puts the
             // integer x (|x| <= 32767) in the low mantissa bits, so its low
             // half-word IS the int16 result.
@@ -332,16 +358,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     }
                 }
             };
-            const uint32_t tacc = tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN;
-            const int nch = (prm.debug & 4) ? 0 : bn / 16;
-            for (int ch = 0; ch < nch; ch += 2) {  // two TMEM loads in flight per wait
+            const int nld = tail_out ? nch - 1 : nch;
+            for (int ch = 0; ch < nld; ch += 2) {  // two TMEM loads in flight per wait
                 uint32_t va[16], vb[16];
                 tmem_ld_32x32b_x16(tacc + ch * 16, va);
-                if (ch + 1 < nch) tmem_ld_32x32b_x16(tacc + (ch + 1) * 16, vb);
+                if (ch + 1 < nld) tmem_ld_32x32b_x16(tacc + (ch + 1) * 16, vb);
                 tmem_ld_wait();
                 emit(va, ch);
-                if (ch + 1 < nch) emit(vb, ch + 1);
+                if (ch + 1 < nld) emit(vb, ch + 1);
             }
+            if (tail_out) emit(vt, nch - 1);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
@@ -359,7 +385,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     }
 }
 
-// BN: the fewest column tiles of <= 224, then the smallest multiple of 16 covering n.
+// BN: the fewest column tiles of <= 256 (an MMA costs the same for any N <= 256),
+// then the smallest multiple of 16 covering n (less B traffic).
 static int pick_bn_fp4(int n) {
     const int tiles = (n + F4_MAX_BN - 1) / F4_MAX_BN;
     const int per = (n + tiles - 1) / tiles;
