@@ -244,6 +244,8 @@ lowbit_status lowbit_generate(int dist, unsigned long long seed, int matrix_id, 
  * Read-and-reset per-role cycle counters of the CTA-pair kernel (enabled by
  * LOWBIT_DEBUG_PAIR=8 in the environment; see tools/pair_stats.py). */
 int lowbit_debug_pair_stats(unsigned long long* out16);
+/* Same for the fp4 pair kernel (LOWBIT_DEBUG_FP4=8). */
+int lowbit_debug_fp4_stats(unsigned long long* out16);
 
 #ifdef __cplusplus
 }

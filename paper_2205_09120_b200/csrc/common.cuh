@@ -328,6 +328,13 @@ LB_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" 
 template <int N>
 LB_DEV void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
 
+// 32-byte vector store (sm_100: one full sector per thread).
+LB_DEV void stg_v8(void* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 LB_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 LB_DEV bool elect_one() { return lane_id() == 0; }
 

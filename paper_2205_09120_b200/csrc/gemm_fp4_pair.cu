@@ -35,13 +35,20 @@ namespace lb {
 constexpr int F4_BM = 128;           // A rows per CTA (256 per pair)
 constexpr int F4_BK = 256;           // depth per k-block (128 bytes of packed e2m1)
 constexpr int F4_MAX_BN = 256;       // pair UMMA N (f32 accumulator columns per buffer)
-#ifndef LOWBIT_F4_STAGES
-#define LOWBIT_F4_STAGES 4
+#ifndef LOWBIT_F4_A_STAGES
+#define LOWBIT_F4_A_STAGES 4
+#endif
+#ifndef LOWBIT_F4_B_STAGES
+#define LOWBIT_F4_B_STAGES 4
 #endif
 #ifndef LOWBIT_F4_RAW_KB
 #define LOWBIT_F4_RAW_KB 64
 #endif
-constexpr int F4_STAGES = LOWBIT_F4_STAGES;  // shared A/B ring
+// A (converter output) and B (TMA) rings.  Equal depths share one release
+// barrier (one commit per k-block); a sweep of (A, B) depths in
+// {(2..5) x (3..6)} on config 5 put (4, 4) first, ahead of deeper B rings.
+constexpr int F4_A_ST = LOWBIT_F4_A_STAGES, F4_B_ST = LOWBIT_F4_B_STAGES;
+constexpr bool F4_SHARED_RING = F4_A_ST == F4_B_ST;
 constexpr int F4_THREADS = 480;
 constexpr int F4_W_RAW = 12, F4_W_B = 13, F4_W_MMA = 14;
 constexpr int F4_A_BYTES = F4_BM * 128;       // 16 KB
@@ -61,7 +68,7 @@ constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp pe
 // (buffer b) reads them from buffer 1-b's tail, which the epilogue of tile
 // i-1 drains first and then overwrites with scales (sf_ready[1-b]).
 constexpr uint32_t F4_SF_OFF = 248;
-constexpr int F4_SMEM = 1024 + F4_STAGES * (F4_A_BYTES + F4_B_BYTES) + F4_RAW_RING + 4 * 2 * F4_EPI_BYTES + 1024;
+constexpr int F4_SMEM = 1024 + F4_A_ST * F4_A_BYTES + F4_B_ST * F4_B_BYTES + F4_RAW_RING + 4 * 2 * F4_EPI_BYTES + 1024;
 static_assert(F4_SMEM <= 227 * 1024, "fp4 pair kernel exceeds shared memory");
 
 struct Fp4Params {
@@ -73,6 +80,13 @@ struct Fp4Params {
     int resident;  // raw A planes stay in the ring across the n tiles of an m tile (m_major only)
     int debug;  // timing experiments only (results invalid): 1 converters skip the expansion, 2 no MMAs
 };
+
+// Role timing for profiling experiments (LOWBIT_DEBUG_FP4 bit 3): cycle
+// counters summed over CTAs, read by lowbit_debug_fp4_stats.
+__device__ unsigned long long g_fp4_stats[16];
+#define F4_T0() const long long _t0 = (prm.debug & 8) ? clock64() : 0
+#define F4_ACC(var) \
+    if (prm.debug & 8) var += clock64() - _t0
 
 // One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1.
 template <bool A_TER>
@@ -98,22 +112,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = sA + F4_STAGES * F4_A_BYTES;
-    uint8_t* sRaw = sB + F4_STAGES * F4_B_BYTES;
+    uint8_t* sB = sA + F4_A_ST * F4_A_BYTES;
+    uint8_t* sRaw = sB + F4_B_ST * F4_B_BYTES;
     uint8_t* sEpi = sRaw + F4_RAW_RING;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * 2 * F4_EPI_BYTES);
     constexpr uint32_t RS = f4_raw_stages(A_TER);
     constexpr uint32_t RAW_SLOT = A_TER ? 2 * F4_RAW_PLANE : F4_RAW_PLANE;
-    static_assert(RS <= 16 && F4_STAGES <= 8, "barrier table sizes");
+    static_assert(RS <= 16 && F4_A_ST <= 8 && F4_B_ST <= 8, "barrier table sizes");
     uint64_t* raw_full = bars;                       // local: raw planes landed            [raw]
     uint64_t* raw_empty = bars + 16;                 // local: 4 converter warps read them  [raw]
-    uint64_t* b_full = bars + 32;                    // leader: both halves of B landed     [ab]
-    uint64_t* a_ready = bars + 40;                   // leader: 8 converter warps done      [ab]
-    uint64_t* ab_empty = bars + 48;                  // local: pair MMAs done with the slot [ab]
-    uint64_t* tmem_full = bars + 56;                 // local: accumulator ready (2)
-    uint64_t* tmem_empty = bars + 58;                // leader: 8 epilogue warps drained (2)
-    uint64_t* sf_ready = bars + 60;                  // leader: scales in buffer c's tail (8 warps) (2)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 62);
+    uint64_t* b_full = bars + 32;                    // leader: both halves of B landed     [b]
+    uint64_t* a_ready = bars + 40;                   // leader: 8 converter warps done      [a]
+    uint64_t* a_empty = bars + 48;                   // local: pair MMAs done with A slot   [a]
+    uint64_t* b_empty = bars + 56;                   // local: pair MMAs done with B slot   [b]
+    uint64_t* tmem_full = bars + 64;                 // local: accumulator ready (2)
+    uint64_t* tmem_empty = bars + 66;                // leader: 8 epilogue warps drained (2)
+    uint64_t* sf_ready = bars + 68;                  // leader: scales in buffer c's tail (8 warps) (2)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 70);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -143,10 +158,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mbar_init(&raw_full[s], 1);
             mbar_init(&raw_empty[s], 4);
         }
-        for (int s = 0; s < F4_STAGES; ++s) {
+        for (int s = 0; s < F4_B_ST; ++s) {
             mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < F4_A_ST; ++s) {
             mbar_init(&a_ready[s], 8);
-            mbar_init(&ab_empty[s], 1);
+            mbar_init(&a_empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
@@ -198,8 +216,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 tile_of(i, mt, nt);
                 const int brow = nt * bn + (int)rank * bnh;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
-                    const uint32_t st = t % F4_STAGES;
-                    mbar_wait_sleep(&ab_empty[st], ((t / F4_STAGES) & 1) ^ 1);
+                    const uint32_t st = t % F4_B_ST;
+                    mbar_wait_sleep(F4_SHARED_RING ? &a_empty[st] : &b_empty[st], ((t / F4_B_ST) & 1) ^ 1);
                     if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
                     tma_load_2d_pair(smem_u32(sB + st * F4_B_BYTES), &tmap_b, b_full0 + st * 8, kb * 128, brow);
                 }
@@ -212,33 +230,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             uint32_t t = 0;
             int acc = 0;
             uint32_t acc_phase = 0, sf_phase = 0;  // sf_phase bit c: parity of the next wait on sf_ready[c]
+            long long w_a = 0, w_b = 0, w_t = 0, w_s = 0;
+            const long long t_start = clock64();
             for (int i = 0; i < my_tiles; ++i) {
-                mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
-                mbar_wait(&sf_ready[acc ^ 1], (sf_phase >> (acc ^ 1)) & 1);
+                {
+                    F4_T0();
+                    mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
+                    F4_ACC(w_t);
+                }
+                {
+                    F4_T0();
+                    mbar_wait(&sf_ready[acc ^ 1], (sf_phase >> (acc ^ 1)) & 1);
+                    F4_ACC(w_s);
+                }
                 sf_phase ^= 1u << (acc ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
                 const uint32_t sf = tmem_base + (uint32_t)(acc ^ 1) * F4_MAX_BN + F4_SF_OFF;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
-                    const uint32_t st = t % F4_STAGES;
-                    mbar_wait(&a_ready[st], (t / F4_STAGES) & 1);
-                    mbar_wait(&b_full[st], (t / F4_STAGES) & 1);
+                    const uint32_t sa = t % F4_A_ST, sb = t % F4_B_ST;
+                    if (!(prm.debug & 16) || t < (uint32_t)F4_B_ST) {  // debug 16: MMA issue rate (no waits)
+                        {
+                            F4_T0();
+                            mbar_wait(&a_ready[sa], (t / F4_A_ST) & 1);
+                            F4_ACC(w_a);
+                        }
+                        {
+                            F4_T0();
+                            mbar_wait(&b_full[sb], (t / F4_B_ST) & 1);
+                            F4_ACC(w_b);
+                        }
+                    }
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t a_addr = smem_u32(sA + st * F4_A_BYTES);
-                        const uint32_t b_addr = smem_u32(sB + st * F4_B_BYTES);
+                        const uint32_t a_addr = smem_u32(sA + sa * F4_A_BYTES);
+                        const uint32_t b_addr = smem_u32(sB + sb * F4_B_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)  // K = 64 per MMA = 32 bytes
                             if (!(prm.debug & 2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                            umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf, (kb | kk) != 0);
-                        umma_commit_pair(&ab_empty[st], 0x3);
+                        umma_commit_pair(&a_empty[sa], 0x3);
+                        if (!F4_SHARED_RING) umma_commit_pair(&b_empty[sb], 0x3);
                     }
                     __syncwarp();
                 }
                 if (lane == 0) umma_commit_pair(&tmem_full[acc], 0x3);
                 __syncwarp();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            if ((prm.debug & 8) && lane == 0) {
+                atomicAdd(&g_fp4_stats[0], (unsigned long long)w_a);
+                atomicAdd(&g_fp4_stats[1], (unsigned long long)w_b);
+                atomicAdd(&g_fp4_stats[2], (unsigned long long)w_t);
+                atomicAdd(&g_fp4_stats[3], (unsigned long long)(clock64() - t_start));
+                atomicAdd(&g_fp4_stats[11], (unsigned long long)w_s);
+                atomicAdd(&g_fp4_stats[12], (unsigned long long)t);
             }
         }
     } else if (warp < 8) {
@@ -250,15 +297,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         const uint32_t kbs = (uint32_t)prm.kblocks, nts = (uint32_t)prm.n_tiles;
         const uint32_t total = (uint32_t)my_tiles * kbs;
         const uint32_t rsw = (uint32_t)(r >> 2) & 1;  // TMA SWIZZLE_32B on the raw rows
+        long long w_raw = 0, w_slot = 0, w_work = 0;
+        const long long t_start = clock64();
         for (uint32_t t = g; t < total; t += 2) {
             // raw load index of this k-block: resident rings load once per m tile
             const uint32_t seq = t / kbs, kb = t - seq * kbs;
             const uint32_t nt = seq % nts;
             const uint32_t u = prm.resident ? (seq / nts) * kbs + kb : t;
             const bool release = !prm.resident || nt == nts - 1;
-            const uint32_t rs = u % RS, st = t % F4_STAGES;
-            mbar_wait_sleep(&raw_full[rs], (u / RS) & 1);
-            mbar_wait_sleep(&ab_empty[st], ((t / F4_STAGES) & 1) ^ 1);
+            const uint32_t rs = u % RS, st = t % F4_A_ST;
+            {
+                F4_T0();
+                mbar_wait_sleep(&raw_full[rs], (u / RS) & 1);
+                F4_ACC(w_raw);
+            }
+            {
+                F4_T0();
+                mbar_wait_sleep(&a_empty[st], ((t / F4_A_ST) & 1) ^ 1);
+                F4_ACC(w_slot);
+            }
+            F4_T0();
             const uint32_t raw = sRaw_u + rs * RAW_SLOT + r * 32;
             if (prm.debug & 1) goto done;
             {
@@ -286,6 +344,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 if (release) mbar_arrive(&raw_empty[rs]);
                 mbar_arrive_cluster(a_ready0 + st * 8);
             }
+            F4_ACC(w_work);
+        }
+        if ((prm.debug & 8) && lane == 0) {
+            atomicAdd(&g_fp4_stats[4], (unsigned long long)w_raw);
+            atomicAdd(&g_fp4_stats[5], (unsigned long long)w_slot);
+            atomicAdd(&g_fp4_stats[6], (unsigned long long)w_work);
+            atomicAdd(&g_fp4_stats[7], (unsigned long long)(clock64() - t_start));
         }
     } else {
         // ===================== epilogue (both CTAs) =====================
@@ -303,15 +368,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         put_scales(1);  // tile 0 runs on buffer 0
 
         const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
+        const bool vec_ok = ((prm.ldc & 15) == 0) && ((reinterpret_cast<uintptr_t>(prm.c) & 31) == 0);
         const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * 2 * F4_EPI_BYTES;
         int acc = 0;
         uint32_t acc_phase = 0;
         int nbuf = 0;
+        long long w_ep = 0, w_tail = 0;
+        const long long t_start = clock64();
         for (int i = 0; i < my_tiles; ++i) {
             int mt, nt;
             tile_of(i, mt, nt);
             const int row0 = mt * 2 * F4_BM + (int)rank * F4_BM + wq * 32;
-            mbar_wait_sleep(&tmem_full[acc], acc_phase);
+            {
+                F4_T0();
+                mbar_wait_sleep(&tmem_full[acc], acc_phase);
+                F4_ACC(w_ep);
+            }
+            F4_T0();
             tc_fence_after();
             const uint32_t tacc = tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN;
             const int nch = (prm.debug & 4) ? 0 : bn / 16;
@@ -323,6 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 tmem_ld_wait();
             }
             put_scales(acc);
+            F4_ACC(w_tail);
             // f32 -> int16 without F2I (quarter rate): x + 1.5 * 2^23 puts the
             // integer x (|x| <= 32767) in the low mantissa bits, so its low
             // half-word IS the int16 result.
@@ -352,9 +426,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     const int row = row0 + lane;
                     if (row < prm.m) {
                         int16_t* crow = prm.c + (long long)row * prm.ldc;
+                        if (vec_ok && col0 + 16 <= prm.n) {  // one full 32-byte sector per lane
+                            stg_v8(crow + col0, h);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (col0 + j < prm.n) crow[col0 + j] = (int16_t)(h[j >> 1] >> (16 * (j & 1)));
+                            for (int j = 0; j < 16; ++j)
+                                if (col0 + j < prm.n) crow[col0 + j] = (int16_t)(h[j >> 1] >> (16 * (j & 1)));
+                        }
                     }
                 }
             };
@@ -374,6 +452,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (prm.tma_store && lane == 0) bulk_wait<0>();
+        if ((prm.debug & 8) && lane == 0) {
+            atomicAdd(&g_fp4_stats[8], (unsigned long long)w_ep);
+            atomicAdd(&g_fp4_stats[9], (unsigned long long)(clock64() - t_start));
+            atomicAdd(&g_fp4_stats[10], (unsigned long long)w_tail);
+        }
     }
 
     tc_fence_before();
@@ -384,6 +467,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         tmem_dealloc_pair<512>(tmem_base);
     }
 }
+
+}  // namespace lb
+
+extern "C" int lowbit_debug_fp4_stats(unsigned long long* out16) {
+    if (cudaMemcpyFromSymbol(out16, lb::g_fp4_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(lb::g_fp4_stats, z, sizeof z) != cudaSuccess) return 1;
+    return 0;
+}
+
+namespace lb {
 
 // BN: the fewest column tiles of <= 256 (an MMA costs the same for any N <= 256),
 // then the smallest multiple of 16 covering n (less B traffic).
@@ -422,6 +516,11 @@ lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a
     prm.ldc = ldc;
     prm.c = c;
     prm.tma_store = ((ldc * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    static const bool direct_epi = [] {
+        const char* e = getenv("LOWBIT_FP4_EPI");
+        return e && e[0] == 'd';
+    }();
+    if (direct_epi) prm.tma_store = 0;
     // resident raw ring: the whole depth fits, and each k-block is always
     // handled by the same converter group (even k-block count) so its last
     // reader is the one that frees it

@@ -1,8 +1,10 @@
-# usage: VARS="lib1 lib2" DBG="0 5" bash tools/fp4_variants.sh
+# usage: VARS="lib1 lib2" DBG="0 5" REPS=3 bash tools/fp4_variants.sh  (tuning experiments)
+for R in $(seq ${REPS:-1}); do
 for V in default ${VARS}; do
   for D in ${DBG:-0}; do
     if [ "$V" = default ]; then unset LOWBIT_LIB; else export LOWBIT_LIB=$PWD/variants/$V.so; fi
-    r=$(LOWBIT_DEBUG_FP4=$D python bench.py --steps ${STEPS:-20} --warmup 3 --layout nibbles --config ${CFG:-c5} --no-cpu-baseline --no-e2e --no-extra | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step'],4), d['clocks']['sm_mhz'], d['clocks'].get('samples'))")
+    r=$(LOWBIT_DEBUG_FP4=$D M=${M:-1048576} NS=${NS:-1024} python tools/fp4_shape_sweep.py | tr '\n' ' ')
     echo "$V debug=$D $r"
   done
+done
 done
