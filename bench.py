@@ -245,9 +245,10 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "bitserial"])
-    ap.add_argument("--layout", default="lanes", choices=["nibbles", "lanes", "reference"],
-                    help="A plane layout written by the (untimed) encode: the B200 lane-interleaved layout or "
-                         "the reference bit order")
+    ap.add_argument("--layout", default="nibbles", choices=["nibbles", "lanes", "reference"],
+                    help="A plane layout written by the (untimed) encode: nibbles -> fp4 (kind::mxf4) tensor-core "
+                         "kernel, lanes -> int8 (kind::i8) kernel, reference -> int8 kernel on the reference bit "
+                         "order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-config side measurements")
@@ -394,13 +395,22 @@ def main():
                   "collective": "torch.distributed.gather (NCCL) of int16 shards as bytes"}
         del full
     pk = peaks()
-    tensor_peak = 2.0 * pk["bf16_tflops"]  # dense int8 tcgen05 = 2x bf16 per SM-clock (4.5 vs 2.25 PF spec)
     achieved = ops_rank / (kernel_ms_avg * 1e-3) / 1e12
-    traffic = load_traffic().get(f"{args.config}:{'tensor' if chosen == lb.KERNEL_TENSOR else 'bitserial'}")
-    if chosen == lb.KERNEL_TENSOR:
+    kkey = {2: "fp4", 1: "tensor", 0: "tensor"}[layout] if chosen == lb.KERNEL_TENSOR else "bitserial"
+    traffic = load_traffic().get(f"{args.config}:{kkey}")
+    if chosen == lb.KERNEL_TENSOR and layout == 2:
+        # dense fp4 tcgen05 = 4x bf16 per SM-clock (9 vs 2.25 PF spec), scaled from the measured bf16 burst
+        tensor_peak = 4.0 * pk["bf16_tflops"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TOP/s",
                 "frac": achieved / tensor_peak, "traffic": traffic,
-                "kernel": "gemm_tc_kernel (tcgen05.mma kind::i8)",
+                "kernel": "gemm_fp4_pair_kernel (tcgen05.mma.cta_group::2 kind::mxf4, unit block scales)",
+                "peak_source": f"4 x bf16 dense {pk['bf16_tflops']} TFLOP/s (fp4 = 4x bf16 rate), {pk['source']}",
+                "algorithmic_ops_per_launch": ops_rank}
+    elif chosen == lb.KERNEL_TENSOR:
+        tensor_peak = 2.0 * pk["bf16_tflops"]  # dense int8 tcgen05 = 2x bf16 per SM-clock (4.5 vs 2.25 PF spec)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TOP/s",
+                "frac": achieved / tensor_peak, "traffic": traffic,
+                "kernel": "gemm_tc_pair_kernel (tcgen05.mma.cta_group::2 kind::i8)",
                 "peak_source": f"2 x bf16 dense {pk['bf16_tflops']} TFLOP/s, {pk['source']}",
                 "algorithmic_ops_per_launch": ops_rank}
     else:
@@ -425,13 +435,17 @@ def main():
             "metric": f"low-bit GeMM TOPS (MAC=2 ops), {MODE_NAME[mode]} {args.config}",
             "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u8 bit-planes in, int8 tensor-core MMA, int32 accumulate, int16 out",
+            "dtype": ("u8 bit-planes in, packed e2m1 (fp4) tensor-core MMA with unit block scales, f32 accumulate "
+                      "(exact: |partial sums| <= 32767), int16 out" if layout == 2 else
+                      "u8 bit-planes in, int8 tensor-core MMA, int32 accumulate, int16 out"),
             "data": "synthetic (counter-based splitmix64 generator, BASELINE.json distributions)",
             "config": {"workload": f"{args.config}: {MODE_NAME[mode]} GeMM M={M} N={N} K={K} int16 C, "
                                    f"A rows sharded over {world} GPU(s), B replicated",
                        "global_rows": M, "rows_per_rank": M // world, "l2": "flushed (256 MiB write) between steps",
                        "kernel": {1: "bitserial", 2: "tensor"}.get(chosen, str(chosen)),
-                       "a_layout": "lanes (B200 lane-interleaved bit planes from K1)" if layout else "reference",
+                       "a_layout": {2: "nibbles (B200 nibble-interleaved bit planes from K1)",
+                                    1: "lanes (B200 lane-interleaved bit planes from K1)",
+                                    0: "reference"}[layout],
                        "parallelism": f"row-shard x{world}"},
             "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "gather": gather, "per_config": extra,
@@ -484,23 +498,25 @@ def side_configs(lb, torch, flush, pk):
     tensor_peak = 2.0 * pk["bf16_tflops"]
     popc = lambda mode: 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
     kernels = (("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL))
+    fp4_peak = 4.0 * pk["bf16_tflops"]
     for name in ("c1", "c3"):
         mode, M, N, K, da, db, seed = CONFIGS[name]
         a = lb.generate(da, seed, 0, M, K)
-        # tensor kernels read the B200 lane-interleaved planes, the bit-serial kernel the reference ones
-        planes = {kid: (lb.encode_binary(a, layout=lay) if mode == 0 else lb.encode_ternary(a, layout=lay))
-                  for kid, lay in ((lb.KERNEL_TENSOR, 1), (lb.KERNEL_BITSERIAL, 0))}
+        # the int8 tensor kernel reads lane-interleaved planes, the fp4 one nibble-interleaved planes,
+        # the bit-serial kernel the reference ones
+        planes = {kn: (lb.encode_binary(a, layout=lay) if mode == 0 else lb.encode_ternary(a, layout=lay))
+                  for kn, lay in (("tensor", 1), ("bitserial", 0), ("tensor_fp4", 2))}
         b = lb.generate(db, seed, 1, K, N)
         w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)))
         c = torch.empty((M, N), dtype=torch.int16, device="cuda")
         res = {}
-        for kn, kid in kernels:
-            f = lambda: lb.gemm_lowbit(mode, planes[kid], w, (M, N, K), kernel=kid, out=c)
+        for kn, kid in kernels + (("tensor_fp4", lb.KERNEL_TENSOR),):
+            f = lambda: lb.gemm_lowbit(mode, planes[kn], w, (M, N, K), kernel=kid, out=c)
             ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
             tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
-            res[kn] = {"ms": ms, "TOPS": tops,
-                       "frac": tops / (tensor_peak if kn == "tensor" else popc(mode)),
-                       "bound": "tensor" if kn == "tensor" else "popc"}
+            peak = {"tensor": tensor_peak, "tensor_fp4": fp4_peak}.get(kn) or popc(mode)
+            res[kn] = {"ms": ms, "TOPS": tops, "frac": tops / peak,
+                       "bound": "popc" if kn == "bitserial" else "tensor"}
         res["auto"] = {1: "bitserial", 2: "tensor"}[lb.select_kernel(mode, M, N, K)]
         res["timing"] = "cuda graph replay" if name == "c1" else "events, L2 flushed"
         out[name] = res
@@ -568,7 +584,7 @@ def side_configs(lb, torch, flush, pk):
     # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
     planes = lb.empty_planes(1048576, 2048, True)
     eb = 1048576 * 2048 + 2 * 1048576 * planes.pitch
-    for lay, name in ((1, "k1_encode_c5_lanes"), (0, "k1_encode_c5_reference_layout")):
+    for lay, name in ((2, "k1_encode_c5_nibbles"), (1, "k1_encode_c5_lanes"), (0, "k1_encode_c5_reference_layout")):
         enc = lambda: L.check(L.lib.lowbit_encode_ex(1, lay, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,
                                                      C.c_void_p(planes.plane0.data_ptr()),
                                                      C.c_void_p(planes.plane1.data_ptr()), planes.pitch, None, st))
