@@ -1,0 +1,113 @@
+// Microbenchmark: back-to-back tcgen05.mma issue rate (operands are whatever
+// is in shared memory / TMEM; results discarded).  One persistent CTA (or CTA
+// pair) per SM, one thread issues ITERS MMAs, commit + wait at the end.
+// Reports cycles per MMA and the implied TOPS at the measured clock.
+#include <cstdio>
+#include <cstdint>
+#include "../../paper_2205_09120_b200/csrc/common.cuh"
+using namespace lb;
+
+template <int KIND, int PAIR>  // KIND 0 = i8 (K=32), 1 = mxf4 (K=64)
+__global__ void __launch_bounds__(128, 1) rate_kernel(int n, int iters, unsigned long long* out, int fill, int opts) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    // operands: zeros (fill 0) or random {-1, 0, +1} codes (fill 1)
+    for (int i = threadIdx.x; i < 4 * 32768 / 4; i += blockDim.x) {
+        uint32_t h = (uint32_t)(i * 2654435761u) ^ (blockIdx.x * 0x9E3779B9u);
+        h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+        uint32_t w = 0;
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t r = (h >> (4 * j)) & 3;
+            const uint32_t code = KIND ? (r == 1 ? 0x2u : r == 2 ? 0xAu : 0u) : 0u;
+            w |= code << (4 * j);
+        }
+        if (!KIND) w = ((h & 0x03030303u) == 0 ? 0 : (h & 0x01010101u) * 0xFFu) ^ (h & 0x01010101u);
+        reinterpret_cast<uint32_t*>(smem)[i] = fill ? w : 0u;
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __shared__ uint32_t tslot;
+    __shared__ uint64_t bar, bar2;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_barrier_init(); }
+    if (warp == 0) { if (PAIR) tmem_alloc_pair<512>(&tslot); else tmem_alloc<512>(&tslot); }
+    tc_fence_before();
+    if (PAIR) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tslot;
+    // zero scales region: fill cols 448.. with 0x7F
+    {
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        for (uint32_t c = 448; c < 512; c += 16) tmem_st_32x32b_x16_fill(tb + lane_base + c, 0x7F7F7F7Fu);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    if (PAIR) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const bool leader = !PAIR || cluster_ctarank() == 0;
+    long long t0 = 0, t1 = 0;
+    if (leader && threadIdx.x == 0) {
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+        const uint32_t M = PAIR ? 256 : 128;
+        const uint32_t id = KIND ? idesc_mxf4(M, n) : idesc_i8(M, n);
+        t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            // opts 1: cycle over 4 stages of (16 KB A, 16 KB B); opts 2: commit every 4 MMAs
+            const uint32_t stage = (opts & 1) ? ((i >> 2) & 3) * 32768u : 0u;
+            const uint64_t ad = umma_desc_k_sw128((opts & 1) ? smem_u32(smem) + stage + (i & 3) * 32 : a + (i & 3) * 32);
+            const uint64_t bd = umma_desc_k_sw128((opts & 1) ? smem_u32(smem) + stage + 16384 + (i & 3) * 32 : b + (i & 3) * 32);
+            if ((opts & 2) && (i & 3) == 0 && i) { if (PAIR) umma_commit_pair(&bar2, 0x3); else umma_commit(&bar2); }
+            if (KIND == 1) {
+                if (PAIR) umma_mxf4_pair(tb, ad, bd, id, tb + 448, tb + 448, 1);
+                else asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                  "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+                                  ::"r"(tb), "l"(ad), "l"(bd), "r"(id), "r"(1), "r"(tb + 448), "r"(tb + 448) : "memory");
+            } else {
+                if (PAIR) umma_i8_pair(tb, ad, bd, id, 1);
+                else umma_i8(tb, ad, bd, id, 1);
+            }
+        }
+        if (PAIR) umma_commit_pair(&bar, 0x1); else umma_commit(&bar);
+        mbar_wait(&bar, 0);
+        t1 = clock64();
+        out[blockIdx.x] = (unsigned long long)(t1 - t0);
+    }
+    tc_fence_before();
+    if (PAIR) cluster_sync(); else __syncthreads();
+    if (warp == 0) { tc_fence_after(); if (PAIR) tmem_dealloc_pair<512>(tb); else tmem_dealloc<512>(tb); }
+}
+
+template <int KIND, int PAIR>
+void run(int n, int iters, int fill, int opts = 0) {
+    auto k = rate_kernel<KIND, PAIR>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    unsigned long long* d; cudaMalloc(&d, 148 * 8); cudaMemset(d, 0, 148 * 8);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = 148; cfg.blockDim = 128; cfg.dynamicSmemBytes = 131072;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = PAIR ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaLaunchKernelEx(&cfg, k, n, iters / 10, d, fill, opts);  // warm
+    cudaEventRecord(e0);
+    cudaLaunchKernelEx(&cfg, k, n, iters, d, fill, opts);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long h[148]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    unsigned long long mx = 0; int cnt = 0;
+    for (int i = 0; i < 148; ++i) if (h[i]) { mx = h[i] > mx ? h[i] : mx; ++cnt; }
+    const double M = PAIR ? 256 : 128, K = KIND ? 64 : 32;
+    const double ops = 2.0 * M * n * K * iters * (PAIR ? 74 : 148);
+    printf("opts=%d %s %s %s N=%d: %s %.1f cycles/MMA (issuers %d), %.3f ms -> %.0f TOPS, clock %.2f GHz\n",
+           opts, fill ? "random" : "zeros ", KIND ? "mxf4" : "i8  ", PAIR ? "pair" : "1cta", n, cudaGetErrorString(err), (double)mx / iters, cnt, ms,
+           ops / (ms * 1e-3) / 1e12, (double)mx / (ms * 1e-3) / 1e9);
+    cudaFree(d);
+}
+
+int main() {
+    const int it = 200000;
+    for (int opts : {0, 1, 2, 3}) run<1, 1>(256, it, 1, opts);
+    for (int opts : {0, 3}) run<1, 1>(208, it, 1, opts);
+    return 0;
+}
