@@ -61,6 +61,10 @@ constexpr int F4_RAW_PLANE = F4_BM * 32;      // 4 KB: 128 rows x 256 bits
 constexpr int F4_RAW_RING = LOWBIT_F4_RAW_KB * 1024;
 __host__ __device__ constexpr int f4_raw_stages(bool ter) { return LOWBIT_F4_RAW_KB / (ter ? 8 : 4); }
 constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp per buffer
+#ifndef LOWBIT_F4_EPI_BUFS
+#define LOWBIT_F4_EPI_BUFS 4
+#endif
+constexpr int F4_EPI_BUFS = LOWBIT_F4_EPI_BUFS;  // TMA-store staging buffers per epilogue warp
 // Scale factors.  An fp4 MMA costs the same for any N <= 256 (measured), so
 // tiles are 256 wide, and two f32 accumulators fill all 512 TMEM columns.
 // The unit scales (SFA and SFB share one 8-column block of 0x7F bytes) live
@@ -68,8 +72,18 @@ constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp pe
 // (buffer b) reads them from buffer 1-b's tail, which the epilogue of tile
 // i-1 drains first and then overwrites with scales (sf_ready[1-b]).
 constexpr uint32_t F4_SF_OFF = 248;
-constexpr int F4_SMEM = 1024 + F4_A_ST * F4_A_BYTES + F4_B_ST * F4_B_BYTES + F4_RAW_RING + 4 * 2 * F4_EPI_BYTES + 1024;
-static_assert(F4_SMEM <= 227 * 1024, "fp4 pair kernel exceeds shared memory");
+// A-resident variant (AR): when k <= 2048 (<= 8 k-blocks) the converted fp4
+// A of a whole m tile (128 rows x 1 KB per CTA) stays in shared memory for
+// all n tiles of that m tile: the converters run once per m tile instead of
+// once per (m, n) tile, and the raw planes only stream through a 16 KB ring.
+constexpr int F4_AR_SLOTS = 8;
+constexpr int F4_AR_RAW = 16 * 1024;
+__host__ __device__ constexpr int f4_smem_bytes(bool ar) {
+    return 1024 + (ar ? F4_AR_SLOTS : F4_A_ST) * F4_A_BYTES + F4_B_ST * F4_B_BYTES + (ar ? F4_AR_RAW : F4_RAW_RING) +
+           4 * F4_EPI_BUFS * F4_EPI_BYTES + 1024;
+}
+static_assert(f4_smem_bytes(false) <= 227 * 1024 && f4_smem_bytes(true) <= 227 * 1024,
+              "fp4 pair kernel exceeds shared memory");
 
 struct Fp4Params {
     int m, n, kblocks, bn, m_tiles, n_tiles;
@@ -78,6 +92,7 @@ struct Fp4Params {
     int tma_store;
     int m_major;   // schedule: 1 = each pair owns whole m tiles (all n tiles back to back)
     int resident;  // raw A planes stay in the ring across the n tiles of an m tile (m_major only)
+    int a_res;     // AR variant (launch selects the template; recorded for the host only)
     int debug;  // timing experiments only (results invalid): 1 converters skip the expansion, 2 no MMAs
 };
 
@@ -104,7 +119,7 @@ __device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) 
     sts_v4(dst, o[0], o[1], o[2], o[3]);
 }
 
-template <bool A_TER>
+template <bool A_TER, bool AR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     gemm_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
                          const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_c,
@@ -112,13 +127,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = sA + F4_A_ST * F4_A_BYTES;
+    constexpr int A_SLOTS = AR ? F4_AR_SLOTS : F4_A_ST;
+    constexpr bool SHARED = !AR && F4_SHARED_RING;  // one release barrier for the A and B slots
+    uint8_t* sB = sA + A_SLOTS * F4_A_BYTES;
     uint8_t* sRaw = sB + F4_B_ST * F4_B_BYTES;
-    uint8_t* sEpi = sRaw + F4_RAW_RING;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * 2 * F4_EPI_BYTES);
-    constexpr uint32_t RS = f4_raw_stages(A_TER);
+    uint8_t* sEpi = sRaw + (AR ? F4_AR_RAW : F4_RAW_RING);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * F4_EPI_BUFS * F4_EPI_BYTES);
     constexpr uint32_t RAW_SLOT = A_TER ? 2 * F4_RAW_PLANE : F4_RAW_PLANE;
-    static_assert(RS <= 16 && F4_A_ST <= 8 && F4_B_ST <= 8, "barrier table sizes");
+    constexpr uint32_t RS = AR ? F4_AR_RAW / RAW_SLOT : f4_raw_stages(A_TER);
+    static_assert(RS <= 16 && A_SLOTS <= 8 && F4_B_ST <= 8, "barrier table sizes");
     uint64_t* raw_full = bars;                       // local: raw planes landed            [raw]
     uint64_t* raw_empty = bars + 16;                 // local: 4 converter warps read them  [raw]
     uint64_t* b_full = bars + 32;                    // leader: both halves of B landed     [b]
@@ -162,7 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mbar_init(&b_full[s], 1);
             mbar_init(&b_empty[s], 1);
         }
-        for (int s = 0; s < F4_A_ST; ++s) {
+        for (int s = 0; s < A_SLOTS; ++s) {
             mbar_init(&a_ready[s], 8);
             mbar_init(&a_empty[s], 1);
         }
@@ -217,7 +234,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 const int brow = nt * bn + (int)rank * bnh;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t st = t % F4_B_ST;
-                    mbar_wait_sleep(F4_SHARED_RING ? &a_empty[st] : &b_empty[st], ((t / F4_B_ST) & 1) ^ 1);
+                    mbar_wait_sleep(SHARED ? &a_empty[st] : &b_empty[st], ((t / F4_B_ST) & 1) ^ 1);
+                    if ((prm.debug & 64) && (i & 1)) {  // timing experiment: half the B traffic (results invalid)
+                        if (leader) mbar_arrive(&b_full[st]);
+                        continue;
+                    }
                     if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
                     tma_load_2d_pair(smem_u32(sB + st * F4_B_BYTES), &tmap_b, b_full0 + st * 8, kb * 128, brow);
                 }
@@ -233,6 +254,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             long long w_a = 0, w_b = 0, w_t = 0, w_s = 0;
             const long long t_start = clock64();
             for (int i = 0; i < my_tiles; ++i) {
+                int mt_, nt_;
+                tile_of(i, mt_, nt_);
+                const uint32_t mgen = (uint32_t)(i / prm.n_tiles);  // AR: this pair's m-tile generation
+                const bool first_nt = nt_ == 0, last_nt = nt_ == prm.n_tiles - 1;
                 {
                     F4_T0();
                     mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
@@ -248,11 +273,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
                 const uint32_t sf = tmem_base + (uint32_t)(acc ^ 1) * F4_MAX_BN + F4_SF_OFF;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
-                    const uint32_t sa = t % F4_A_ST, sb = t % F4_B_ST;
+                    const uint32_t sa = AR ? (uint32_t)kb : t % F4_A_ST, sb = t % F4_B_ST;
                     if (!(prm.debug & 16) || t < (uint32_t)F4_B_ST) {  // debug 16: MMA issue rate (no waits)
-                        {
+                        if (!AR || first_nt) {  // AR: later n tiles reuse the converted A
                             F4_T0();
-                            mbar_wait(&a_ready[sa], (t / F4_A_ST) & 1);
+                            mbar_wait(&a_ready[sa], AR ? (mgen & 1) : (t / F4_A_ST) & 1);
                             F4_ACC(w_a);
                         }
                         {
@@ -270,8 +295,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                             if (!(prm.debug & 2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                            umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf, (kb | kk) != 0);
-                        umma_commit_pair(&a_empty[sa], 0x3);
-                        if (!F4_SHARED_RING) umma_commit_pair(&b_empty[sb], 0x3);
+                        if (!AR || last_nt) umma_commit_pair(&a_empty[sa], 0x3);
+                        if (!SHARED) umma_commit_pair(&b_empty[sb], 0x3);
                     }
                     __syncwarp();
                 }
@@ -299,7 +324,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         const uint32_t rsw = (uint32_t)(r >> 2) & 1;  // TMA SWIZZLE_32B on the raw rows
         long long w_raw = 0, w_slot = 0, w_work = 0;
         const long long t_start = clock64();
-        for (uint32_t t = g; t < total; t += 2) {
+        if (AR) {
+            // one item per (m tile, k-block); kbs is even, so a group always owns
+            // the same k-blocks and its waits on a slot's barriers stay in order
+            const uint32_t items = (uint32_t)(my_tiles / prm.n_tiles) * kbs;
+            for (uint32_t u = g; u < items; u += 2) {
+                const uint32_t mgen = u / kbs, kb = u - mgen * kbs;
+                const uint32_t rs = u % RS;
+                {
+                    F4_T0();
+                    mbar_wait_sleep(&raw_full[rs], (u / RS) & 1);
+                    F4_ACC(w_raw);
+                }
+                const uint32_t raw = sRaw_u + rs * RAW_SLOT + r * 32;
+                const uint4 p0 = lds_v4(raw + (rsw << 4)), p1 = lds_v4(raw + ((rsw ^ 1) << 4));
+                uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0;
+                if (A_TER) {
+                    m0 = lds_v4(raw + F4_RAW_PLANE + (rsw << 4));
+                    m1 = lds_v4(raw + F4_RAW_PLANE + ((rsw ^ 1) << 4));
+                }
+                // free the 16 KB raw ring early: the loads have returned (the dummy
+                // asm consumes them) and are ordered before the TMA refill
+                asm volatile("" ::"r"(p0.x), "r"(p1.w), "r"(m0.x), "r"(m1.w));
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&raw_empty[rs]);
+                {
+                    F4_T0();
+                    mbar_wait_sleep(&a_empty[kb], (mgen & 1) ^ 1);  // last n tile of the previous m tile done
+                    F4_ACC(w_slot);
+                }
+                F4_T0();
+                const uint32_t row = sA_u + kb * F4_A_BYTES + r * 128;
+                const uint32_t sw = (uint32_t)r & 7;  // SW128: chunk c at c ^ (row % 8)
+                fp4_chunk<A_TER>(p0.x, m0.x, row + ((0 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.y, m0.y, row + ((1 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.z, m0.z, row + ((2 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.w, m0.w, row + ((3 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.x, m1.x, row + ((4 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(a_ready0 + kb * 8);
+                F4_ACC(w_work);
+            }
+        }
+        for (uint32_t t = g; !AR && t < total; t += 2) {
             // raw load index of this k-block: resident rings load once per m tile
             const uint32_t seq = t / kbs, kb = t - seq * kbs;
             const uint32_t nt = seq % nts;
@@ -369,7 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
 
         const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
         const bool vec_ok = ((prm.ldc & 15) == 0) && ((reinterpret_cast<uintptr_t>(prm.c) & 31) == 0);
-        const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * 2 * F4_EPI_BYTES;
+        const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * F4_EPI_BUFS * F4_EPI_BYTES;
         int acc = 0;
         uint32_t acc_phase = 0;
         int nbuf = 0;
@@ -409,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 const int col0 = nt * bn + ch * 16;
                 if (prm.tma_store) {
                     const uint32_t buf = epi + (uint32_t)nbuf * F4_EPI_BYTES;
-                    if (lane == 0) bulk_wait_read<1>();
+                    if (lane == 0) bulk_wait_read<F4_EPI_BUFS - 1>();
                     __syncwarp();
                     const uint32_t rowaddr = buf + lane * 32;
                     const uint32_t sw = (uint32_t)(lane >> 2) & 1;  // TMA SWIZZLE_32B
@@ -421,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         tma_store_2d(&tmap_c, buf, col0, row0);
                         bulk_commit();
                     }
-                    nbuf ^= 1;
+                    nbuf = nbuf + 1 == F4_EPI_BUFS ? 0 : nbuf + 1;
                 } else {
                     const int row = row0 + lane;
                     if (row < prm.m) {
@@ -487,16 +559,17 @@ static int pick_bn_fp4(int n) {
     return (per + 15) / 16 * 16;
 }
 
-template <bool A_TER>
+template <bool A_TER, bool AR>
 static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                         const CUtensorMap& mc, const Fp4Params& prm, int pairs, cudaStream_t stream) {
     static bool attr = false;
+    constexpr int smem = f4_smem_bytes(AR);
     if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_pair_kernel<A_TER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         F4_SMEM));
+        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_pair_kernel<A_TER, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem));
         attr = true;
     }
-    gemm_fp4_pair_kernel<A_TER><<<2 * pairs, F4_THREADS, F4_SMEM, stream>>>(mb, ma0, ma1, mc, prm);
+    gemm_fp4_pair_kernel<A_TER, AR><<<2 * pairs, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }
@@ -527,6 +600,12 @@ lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a
     prm.m_major = prm.m_tiles >= num_sms() / 2;
     prm.resident = prm.m_major && prm.kblocks <= f4_raw_stages(a_ternary != 0) &&
                    (prm.kblocks % 2 == 0 || prm.n_tiles == 1);
+    static const int no_ar = [] {
+        const char* e = getenv("LOWBIT_FP4_NO_AR");  // tuning experiments: force the streaming variant
+        return e ? atoi(e) : 0;
+    }();
+    prm.a_res = !no_ar && prm.m_major && prm.n_tiles >= 2 && prm.kblocks <= F4_AR_SLOTS && prm.kblocks % 2 == 0;
+    if (prm.a_res) prm.resident = 1;  // raw planes load once per m tile
     static const int debug = [] {
         const char* e = getenv("LOWBIT_DEBUG_FP4");
         return e ? atoi(e) : 0;
@@ -556,8 +635,11 @@ lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a
     }
     const int work = prm.m_major ? prm.m_tiles : prm.m_tiles * prm.n_tiles;
     const int pairs = work < num_sms() / 2 ? work : num_sms() / 2;
-    return a_ternary ? launch_fp4_variant<true>(mb, ma0, ma1, mc, prm, pairs, stream)
-                     : launch_fp4_variant<false>(mb, ma0, ma1, mc, prm, pairs, stream);
+    if (prm.a_res)
+        return a_ternary ? launch_fp4_variant<true, true>(mb, ma0, ma1, mc, prm, pairs, stream)
+                         : launch_fp4_variant<false, true>(mb, ma0, ma1, mc, prm, pairs, stream);
+    return a_ternary ? launch_fp4_variant<true, false>(mb, ma0, ma1, mc, prm, pairs, stream)
+                     : launch_fp4_variant<false, false>(mb, ma0, ma1, mc, prm, pairs, stream);
 }
 
 }  // namespace lb
