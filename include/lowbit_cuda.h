@@ -63,9 +63,10 @@ typedef enum lowbit_gemm_mode { LOWBIT_BNN = 0, LOWBIT_TNN = 1, LOWBIT_TBN = 2 }
 typedef enum lowbit_kernel {
     LOWBIT_KERNEL_AUTO = 0,
     LOWBIT_KERNEL_BITSERIAL = 1,  /* K2: LOP3 + POPC, int32 registers */
-    LOWBIT_KERNEL_TENSOR = 2,     /* K3: tcgen05.mma kind::i8, int32 TMEM accumulators; CTA pairs
-                                     (cta_group::2, 256-row tiles) when m > 128, else one CTA */
-    LOWBIT_KERNEL_TENSOR_1CTA = 3 /* K3 forced to the single-CTA (cta_group::1) variant */
+    LOWBIT_KERNEL_TENSOR = 2,     /* tensor cores: K5 (tcgen05.mma kind::mxf4, packed e2m1, CTA pairs)
+                                     for REFERENCE and NIBBLES planes; K3 (kind::i8) for LANES planes */
+    LOWBIT_KERNEL_TENSOR_1CTA = 3, /* K3 forced to the single-CTA (cta_group::1) variant */
+    LOWBIT_KERNEL_TENSOR_I8 = 4   /* K3 (kind::i8, int32 TMEM accumulators; CTA pairs when m > 128) */
 } lowbit_kernel;
 
 typedef void* lowbit_stream; /* cudaStream_t */

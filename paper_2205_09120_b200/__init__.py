@@ -12,7 +12,7 @@ Ternary (TNN), ternary-binary (TBN) and binary (BNN) matrix multiplication of
 The C ABI library is mandatory: importing this package fails if it is not built.
 """
 from ._lib import (  # noqa: F401
-    BNN, TNN, TBN, KERNEL_AUTO, KERNEL_BITSERIAL, KERNEL_TENSOR, KERNEL_TENSOR_1CTA, K_MAX16,
+    BNN, TNN, TBN, KERNEL_AUTO, KERNEL_BITSERIAL, KERNEL_TENSOR, KERNEL_TENSOR_1CTA, KERNEL_TENSOR_I8, K_MAX16,
     Error, ZeroInBinaryInput, InvalidCode, OutOfBounds, DepthOverflow, ModeMismatch, ChannelOverflow,
     EmptyOutput, InvalidPlan, CudaError, InvalidArgument, NoDevice, LIB_PATH,
 )

@@ -21,7 +21,7 @@ CHANNEL_OVERFLOW, EMPTY_OUTPUT, CUDA_ERROR, INVALID_ARGUMENT, NO_DEVICE = range(
 # lowbit_gemm_mode (gemm.hpp:24)
 BNN, TNN, TBN = 0, 1, 2
 # lowbit_kernel
-KERNEL_AUTO, KERNEL_BITSERIAL, KERNEL_TENSOR, KERNEL_TENSOR_1CTA = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_BITSERIAL, KERNEL_TENSOR, KERNEL_TENSOR_1CTA, KERNEL_TENSOR_I8 = 0, 1, 2, 3, 4
 K_MAX16 = 32767
 # lowbit_layout
 LAYOUT_REFERENCE, LAYOUT_LANES = 0, 1

@@ -16,7 +16,7 @@ lowbit_status launch_tensor_pair(int a_ternary, int layout, const uint8_t* a0, c
                                  cudaStream_t stream);
 lowbit_status launch_tensor_pair_i8(const int8_t* a, long long lda, int m, int n, int k, const void* weights,
                                     int b_ternary, int16_t* c, long long ldc, cudaStream_t stream);
-lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                               int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                               cudaStream_t stream);
 lowbit_status launch_tensor(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
@@ -165,13 +165,15 @@ extern "C" lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a
             return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: the bit-serial kernel reads REFERENCE-layout planes");
         return lb::launch_bitserial(mode, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     }
-    if (a_layout == LOWBIT_LAYOUT_NIBBLES) {  // fp4 tensor cores (CTA pairs for every m)
-        if (kernel != LOWBIT_KERNEL_TENSOR)
-            return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: NIBBLES planes run on the tensor-core pair kernel only");
-        return lb::launch_fp4_pair(a_ternary, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
-    }
-    if (kernel == LOWBIT_KERNEL_TENSOR && m > 128)
+    if (a_layout == LOWBIT_LAYOUT_NIBBLES && kernel != LOWBIT_KERNEL_TENSOR)
+        return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: NIBBLES planes run on the fp4 tensor-core kernel only");
+    // TENSOR: the fp4 kernel K5 for NIBBLES and REFERENCE planes, the int8 kernel K3 for LANES planes
+    if (kernel == LOWBIT_KERNEL_TENSOR && a_layout != LOWBIT_LAYOUT_LANES)
+        return lb::launch_fp4_pair(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    if ((kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_I8) && m > 128)
         return lb::launch_tensor_pair(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
+    if (kernel == LOWBIT_KERNEL_TENSOR_I8)
+        return lb::launch_tensor(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     if (kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_1CTA)
         return lb::launch_tensor(a_ternary, a_layout, a0, a1, a_pitch, m, n, k, weights, b_ternary, c, ldc, s);
     return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown kernel id");

@@ -104,10 +104,26 @@ __device__ unsigned long long g_fp4_stats[16];
     if (prm.debug & 8) var += clock64() - _t0
 
 // One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1.
-template <bool A_TER>
+// Reference bit order (element j of a word at bit j): byte q of the word ->
+// its 8 bits one per nibble (bit k -> bit 4k).
+__device__ __forceinline__ uint32_t spread8_nibbles(uint32_t b) {
+    uint32_t x = (b | (b << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return (x | (x << 3)) & 0x11111111u;
+}
+
+// LAYOUT 2 (NIBBLES): ~4.5 integer ops per 8 elements; LAYOUT 0 (REFERENCE
+// planes, the reference's own encoding): ~16 ternary / ~9 binary.
+template <bool A_TER, int LAYOUT>
 __device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) {
     uint32_t o[4];
-    if (A_TER) {
+    if (LAYOUT == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t ps = spread8_nibbles((p >> (8 * q)) & 0xFFu);
+            o[q] = A_TER ? spread8_nibbles((m >> (8 * q)) & 0xFFu) * 10u + (ps << 1) : ps * 8u + 0x22222222u;
+        }
+    } else if (A_TER) {
         o[0] = (m & 0x11111111u) * 10u + ((p << 1) & 0x22222222u);
         o[1] = ((m >> 1) & 0x11111111u) * 10u + (p & 0x22222222u);
         o[2] = ((m >> 2) & 0x11111111u) * 10u + ((p >> 1) & 0x22222222u);
@@ -119,7 +135,7 @@ __device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) 
     sts_v4(dst, o[0], o[1], o[2], o[3]);
 }
 
-template <bool A_TER, bool AR>
+template <bool A_TER, bool AR, int LAYOUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     gemm_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
                          const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_c,
@@ -357,14 +373,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 F4_T0();
                 const uint32_t row = sA_u + kb * F4_A_BYTES + r * 128;
                 const uint32_t sw = (uint32_t)r & 7;  // SW128: chunk c at c ^ (row % 8)
-                fp4_chunk<A_TER>(p0.x, m0.x, row + ((0 ^ sw) << 4));
-                fp4_chunk<A_TER>(p0.y, m0.y, row + ((1 ^ sw) << 4));
-                fp4_chunk<A_TER>(p0.z, m0.z, row + ((2 ^ sw) << 4));
-                fp4_chunk<A_TER>(p0.w, m0.w, row + ((3 ^ sw) << 4));
-                fp4_chunk<A_TER>(p1.x, m1.x, row + ((4 ^ sw) << 4));
-                fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
-                fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
-                fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p0.x, m0.x, row + ((0 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p0.y, m0.y, row + ((1 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p0.z, m0.z, row + ((2 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p0.w, m0.w, row + ((3 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p1.x, m1.x, row + ((4 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p1.y, m1.y, row + ((5 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p1.z, m1.z, row + ((6 ^ sw) << 4));
+                fp4_chunk<A_TER, LAYOUT>(p1.w, m1.w, row + ((7 ^ sw) << 4));
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(a_ready0 + kb * 8);
@@ -400,14 +416,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             }
             const uint32_t row = sA_u + st * F4_A_BYTES + r * 128;
             const uint32_t sw = (uint32_t)r & 7;  // SW128: chunk c at c ^ (row % 8)
-            fp4_chunk<A_TER>(p0.x, m0.x, row + ((0 ^ sw) << 4));
-            fp4_chunk<A_TER>(p0.y, m0.y, row + ((1 ^ sw) << 4));
-            fp4_chunk<A_TER>(p0.z, m0.z, row + ((2 ^ sw) << 4));
-            fp4_chunk<A_TER>(p0.w, m0.w, row + ((3 ^ sw) << 4));
-            fp4_chunk<A_TER>(p1.x, m1.x, row + ((4 ^ sw) << 4));
-            fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
-            fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
-            fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p0.x, m0.x, row + ((0 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p0.y, m0.y, row + ((1 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p0.z, m0.z, row + ((2 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p0.w, m0.w, row + ((3 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p1.x, m1.x, row + ((4 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p1.y, m1.y, row + ((5 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p1.z, m1.z, row + ((6 ^ sw) << 4));
+            fp4_chunk<A_TER, LAYOUT>(p1.w, m1.w, row + ((7 ^ sw) << 4));
             }
         done:
             fence_proxy_async_smem();
@@ -559,23 +575,23 @@ static int pick_bn_fp4(int n) {
     return (per + 15) / 16 * 16;
 }
 
-template <bool A_TER, bool AR>
+template <bool A_TER, bool AR, int LAYOUT>
 static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                         const CUtensorMap& mc, const Fp4Params& prm, int pairs, cudaStream_t stream) {
     static bool attr = false;
     constexpr int smem = f4_smem_bytes(AR);
     if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_pair_kernel<A_TER, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_pair_kernel<A_TER, AR, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem));
         attr = true;
     }
-    gemm_fp4_pair_kernel<A_TER, AR><<<2 * pairs, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
+    gemm_fp4_pair_kernel<A_TER, AR, LAYOUT><<<2 * pairs, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }
 
 // A as NIBBLES-layout bit planes (lowbit_encode_ex layout 2).
-lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
+lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
                               int k, const void* weights, int b_ternary, int16_t* c, long long ldc,
                               cudaStream_t stream) {
     const WeightsLayout L(b_ternary, n, k);
@@ -635,11 +651,14 @@ lowbit_status launch_fp4_pair(int a_ternary, const uint8_t* a0, const uint8_t* a
     }
     const int work = prm.m_major ? prm.m_tiles : prm.m_tiles * prm.n_tiles;
     const int pairs = work < num_sms() / 2 ? work : num_sms() / 2;
-    if (prm.a_res)
-        return a_ternary ? launch_fp4_variant<true, true>(mb, ma0, ma1, mc, prm, pairs, stream)
-                         : launch_fp4_variant<false, true>(mb, ma0, ma1, mc, prm, pairs, stream);
-    return a_ternary ? launch_fp4_variant<true, false>(mb, ma0, ma1, mc, prm, pairs, stream)
-                     : launch_fp4_variant<false, false>(mb, ma0, ma1, mc, prm, pairs, stream);
+#define F4_LAUNCH(TER, AR_, LAY) launch_fp4_variant<TER, AR_, LAY>(mb, ma0, ma1, mc, prm, pairs, stream)
+    if (layout == LOWBIT_LAYOUT_NIBBLES) {
+        if (prm.a_res) return a_ternary ? F4_LAUNCH(true, true, 2) : F4_LAUNCH(false, true, 2);
+        return a_ternary ? F4_LAUNCH(true, false, 2) : F4_LAUNCH(false, false, 2);
+    }
+    if (prm.a_res) return a_ternary ? F4_LAUNCH(true, true, 0) : F4_LAUNCH(false, true, 0);
+    return a_ternary ? F4_LAUNCH(true, false, 0) : F4_LAUNCH(false, false, 0);
+#undef F4_LAUNCH
 }
 
 }  // namespace lb

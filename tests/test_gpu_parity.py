@@ -17,7 +17,9 @@ pytestmark = pytest.mark.gpu
 from oracle.oracle import BNN, TNN, TBN, a_mode_ternary, b_mode_ternary  # noqa: E402
 from tests.golden.make_golden import SMALL_GEMM, mode_dists, sweep_shapes  # noqa: E402
 
-KERNELS = [1, 2, 3]  # LOWBIT_KERNEL_BITSERIAL, LOWBIT_KERNEL_TENSOR (pairs), LOWBIT_KERNEL_TENSOR_1CTA
+# LOWBIT_KERNEL_BITSERIAL, LOWBIT_KERNEL_TENSOR (reference planes -> fp4 K5), LOWBIT_KERNEL_TENSOR_1CTA,
+# LOWBIT_KERNEL_TENSOR_I8 (int8 K3, CTA pairs when m > 128)
+KERNELS = [1, 2, 3, 4]
 
 
 @pytest.fixture(scope="module")
@@ -255,7 +257,7 @@ def _row_col_sum_check(a, b, c):
     assert torch.equal(c_cols, want_cols)
 
 
-@pytest.mark.parametrize("kernel", [2, 3])
+@pytest.mark.parametrize("kernel", [2, 3, 4])
 def test_config3_full(lb, port, golden_configs, kernel):
     m = n = 8192
     k = 4096
@@ -283,10 +285,11 @@ def test_config3_bitserial_sampled(lb, port):
         assert (host(c[r0:r0 + 2]) == want).all()
 
 
-def test_config5_full(lb, port, golden_configs):
+@pytest.mark.parametrize("kernel", [2, 4])
+def test_config5_full(lb, port, golden_configs, kernel):
     m, n, k = 1048576, 1024, 2048
     a, b, ap, w = _device_inputs(lb, TNN, 47, m, n, k, 0, 0)
-    c = lb.gemm_lowbit(TNN, ap, w, (m, n, k), kernel=2)
+    c = lb.gemm_lowbit(TNN, ap, w, (m, n, k), kernel=kernel)
     torch.cuda.synchronize()
     _row_col_sum_check(a, b, c)
     bb = port.generate(0, 47, 1, k, n)
