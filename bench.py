@@ -293,7 +293,7 @@ def main():
     w = lb.prepare_weights(pb)
     c = torch.empty((m, N), dtype=torch.int16, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    chosen = kernel if kernel else lb.select_kernel(mode, m, N, K)
+    chosen = kernel if kernel else (lb.KERNEL_TENSOR if layout == 2 else lb.select_kernel(mode, m, N, K))
 
     def step():
         lb.gemm_lowbit(mode, ap_, w, (m, N, K), kernel=kernel, out=c)
@@ -396,17 +396,23 @@ def main():
         del full
     pk = peaks()
     achieved = ops_rank / (kernel_ms_avg * 1e-3) / 1e12
-    kkey = {2: "fp4", 1: "tensor", 0: "tensor"}[layout] if chosen == lb.KERNEL_TENSOR else "bitserial"
+    fp4 = chosen == lb.KERNEL_TENSOR and layout != 1  # K5 reads NIBBLES and REFERENCE planes, K3 LANES
+    kkey = ("fp4" if fp4 else "tensor") if chosen in (lb.KERNEL_TENSOR, lb.KERNEL_TENSOR_I8) else "bitserial"
     traffic = load_traffic().get(f"{args.config}:{kkey}")
-    if chosen == lb.KERNEL_TENSOR and layout == 2:
+    if fp4:
         # dense fp4 tcgen05 = 4x bf16 per SM-clock (9 vs 2.25 PF spec), scaled from the measured bf16 burst
         tensor_peak = 4.0 * pk["bf16_tflops"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TOP/s",
                 "frac": achieved / tensor_peak, "traffic": traffic,
                 "kernel": "gemm_fp4_pair_kernel (tcgen05.mma.cta_group::2 kind::mxf4, unit block scales)",
                 "peak_source": f"4 x bf16 dense {pk['bf16_tflops']} TFLOP/s (fp4 = 4x bf16 rate), {pk['source']}",
+                # the fp4 pair MMA's own measured issue rate (tools/micro/mma_rate.cu, random operands,
+                # profiles/r01/mma_microbench.txt): a stricter denominator than the bf16-derived peak
+                "mma_issue_peak_measured": {"value": 8843.0, "frac": achieved / 8843.0,
+                                            "source": "tools/micro/mma_rate.cu: 128 cycles per 256x256x64 "
+                                                      "pair MMA at 1.82 GHz"},
                 "algorithmic_ops_per_launch": ops_rank}
-    elif chosen == lb.KERNEL_TENSOR:
+    elif chosen in (lb.KERNEL_TENSOR, lb.KERNEL_TENSOR_I8):
         tensor_peak = 2.0 * pk["bf16_tflops"]  # dense int8 tcgen05 = 2x bf16 per SM-clock (4.5 vs 2.25 PF spec)
         roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TOP/s",
                 "frac": achieved / tensor_peak, "traffic": traffic,
@@ -436,13 +442,14 @@ def main():
             "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": ("u8 bit-planes in, packed e2m1 (fp4) tensor-core MMA with unit block scales, f32 accumulate "
-                      "(exact: |partial sums| <= 32767), int16 out" if layout == 2 else
+                      "(exact: |partial sums| <= 32767), int16 out" if fp4 else
                       "u8 bit-planes in, int8 tensor-core MMA, int32 accumulate, int16 out"),
             "data": "synthetic (counter-based splitmix64 generator, BASELINE.json distributions)",
             "config": {"workload": f"{args.config}: {MODE_NAME[mode]} GeMM M={M} N={N} K={K} int16 C, "
                                    f"A rows sharded over {world} GPU(s), B replicated",
                        "global_rows": M, "rows_per_rank": M // world, "l2": "flushed (256 MiB write) between steps",
-                       "kernel": {1: "bitserial", 2: "tensor"}.get(chosen, str(chosen)),
+                       "kernel": {1: "bitserial", 2: "tensor (fp4 K5)" if fp4 else "tensor (int8 K3)",
+                                  4: "tensor (int8 K3)"}.get(chosen, str(chosen)),
                        "a_layout": {2: "nibbles (B200 nibble-interleaved bit planes from K1)",
                                     1: "lanes (B200 lane-interleaved bit planes from K1)",
                                     0: "reference"}[layout],
@@ -499,25 +506,27 @@ def side_configs(lb, torch, flush, pk):
     popc = lambda mode: 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
     kernels = (("tensor", lb.KERNEL_TENSOR), ("bitserial", lb.KERNEL_BITSERIAL))
     fp4_peak = 4.0 * pk["bf16_tflops"]
+    # (name, A plane layout, kernel id, peak): K5 fp4 from the reference encoding (what AUTO runs) and
+    # from nibble-interleaved planes, K3 int8 from lane-interleaved planes, K2 bit-serial
+    variants = (("tensor_fp4", 0, lb.KERNEL_TENSOR, "fp4"), ("tensor_fp4_nibbles", 2, lb.KERNEL_TENSOR, "fp4"),
+                ("tensor_i8_lanes", 1, lb.KERNEL_TENSOR, "i8"), ("bitserial", 0, lb.KERNEL_BITSERIAL, "popc"))
     for name in ("c1", "c3"):
         mode, M, N, K, da, db, seed = CONFIGS[name]
         a = lb.generate(da, seed, 0, M, K)
-        # the int8 tensor kernel reads lane-interleaved planes, the fp4 one nibble-interleaved planes,
-        # the bit-serial kernel the reference ones
-        planes = {kn: (lb.encode_binary(a, layout=lay) if mode == 0 else lb.encode_ternary(a, layout=lay))
-                  for kn, lay in (("tensor", 1), ("bitserial", 0), ("tensor_fp4", 2))}
+        planes = {lay: (lb.encode_binary(a, layout=lay) if mode == 0 else lb.encode_ternary(a, layout=lay))
+                  for lay in (0, 1, 2)}
         b = lb.generate(db, seed, 1, K, N)
         w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(b) if mode == 1 else lb.encode_binary(b)))
         c = torch.empty((M, N), dtype=torch.int16, device="cuda")
         res = {}
-        for kn, kid in kernels + (("tensor_fp4", lb.KERNEL_TENSOR),):
-            f = lambda: lb.gemm_lowbit(mode, planes[kn], w, (M, N, K), kernel=kid, out=c)
+        for kn, lay, kid, pkind in variants:
+            f = lambda: lb.gemm_lowbit(mode, planes[lay], w, (M, N, K), kernel=kid, out=c)
             ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
             tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
-            peak = {"tensor": tensor_peak, "tensor_fp4": fp4_peak}.get(kn) or popc(mode)
+            peak = {"fp4": fp4_peak, "i8": tensor_peak}.get(pkind) or popc(mode)
             res[kn] = {"ms": ms, "TOPS": tops, "frac": tops / peak,
                        "bound": "popc" if kn == "bitserial" else "tensor"}
-        res["auto"] = {1: "bitserial", 2: "tensor"}[lb.select_kernel(mode, M, N, K)]
+        res["auto"] = {2: "tensor_fp4", 4: "tensor_i8 (reference planes)"}.get(lb.select_kernel(mode, M, N, K))
         res["timing"] = "cuda graph replay" if name == "c1" else "events, L2 flushed"
         out[name] = res
     # c2: the 64-shape TBN sweep (one launch per shape), captured as one graph

@@ -59,7 +59,9 @@ typedef enum lowbit_status {
 typedef enum lowbit_gemm_mode { LOWBIT_BNN = 0, LOWBIT_TNN = 1, LOWBIT_TBN = 2 } lowbit_gemm_mode;
 
 /* Kernel choice for lowbit_gemm.  AUTO consults the static per-shape table
- * (lowbit_select_kernel); the others force one kernel (tests, profiling). */
+ * (lowbit_select_kernel: the int8 kernel for launch-bound shapes under ~1 GOP,
+ * else the fp4 one; NIBBLES planes always run the fp4 kernel); the others
+ * force one kernel (tests, profiling). */
 typedef enum lowbit_kernel {
     LOWBIT_KERNEL_AUTO = 0,
     LOWBIT_KERNEL_BITSERIAL = 1,  /* K2: LOP3 + POPC, int32 registers */

@@ -118,21 +118,19 @@ static lowbit_status validate_gemm(int mode, bool a_ternary, int b_ternary, int 
 }
 
 // Static per-shape kernel table, from B200
-// measurements (profiles/r01, bench.py per_config):
-//   c1 360x96x256      tcgen05 6.7 us   vs bit-serial 12.6 us (graph replay)
-//   c2 sweep (64)      tcgen05 5.0 us   vs bit-serial 10.5 us per shape
-//   c3 8192^2x4096     tcgen05 2.68 POPS vs bit-serial 0.28 POPS (95% of POPC peak)
-//   c4 conv            tcgen05 implicit GeMM 48 us (1.23 POPS) vs K4 + bit-serial 630 us
-//   c5 1Mx1024x2048    tcgen05 2.55-2.69 POPS from bit planes, 3.15 POPS from int8
-// The int8 tensor path wins every measured shape, including the launch-bound
-// ones, so AUTO maps to it; the bit-serial kernel stays selectable (and is the
-// one the grouped small-GeMM launch uses, lowbit_gemm_grouped).
+// measurements (profiles/r01, bench.py per_config), reference-layout planes:
+//   c1 360x96x256      int8 K3 6.4 us, fp4 K5 8.6 us, bit-serial 12.6 us (graph replay)
+//   c2 sweep (64)      int8 K3 5.0 us, fp4 K5 5.7 us, bit-serial 10.4 us per shape
+//   c3 8192^2x4096     fp4 K5 4.04 POPS, int8 K3 2.7 POPS, bit-serial 0.28 POPS (95% of POPC peak)
+//   c5 1Mx1024x2048    fp4 K5 4.73 POPS, int8 K3 2.50 POPS
+// Launch-bound shapes (under ~1 GOP) take the int8 kernel, everything else the
+// fp4 one.  (NIBBLES planes always run K5, LANES planes K3; lowbit_gemm_ex.)
+// The bit-serial kernel stays selectable and is the one the grouped
+// small-GeMM launch uses (lowbit_gemm_grouped).
 extern "C" int lowbit_select_kernel(int mode, int m, int n, int k) {
     (void)mode;
-    (void)m;
-    (void)n;
-    (void)k;
-    return LOWBIT_KERNEL_TENSOR;
+    const double ops = 2.0 * (double)m * (double)n * (double)k;
+    return ops < 1e9 ? LOWBIT_KERNEL_TENSOR_I8 : LOWBIT_KERNEL_TENSOR;
 }
 
 extern "C" lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int a_rows,
@@ -158,7 +156,8 @@ extern "C" lowbit_status lowbit_gemm_ex(int mode, int a_layout, const uint8_t* a
     if (ldc < n) return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: ldc < n");
     if (a_layout != LOWBIT_LAYOUT_REFERENCE && a_layout != LOWBIT_LAYOUT_LANES && a_layout != LOWBIT_LAYOUT_NIBBLES)
         return set_error(LOWBIT_INVALID_ARGUMENT, "gemm: unknown A plane layout");
-    if (kernel == LOWBIT_KERNEL_AUTO) kernel = lowbit_select_kernel(mode, m, n, k);
+    if (kernel == LOWBIT_KERNEL_AUTO)
+        kernel = a_layout == LOWBIT_LAYOUT_NIBBLES ? LOWBIT_KERNEL_TENSOR : lowbit_select_kernel(mode, m, n, k);
     cudaStream_t s = (cudaStream_t)stream;
     if (kernel == LOWBIT_KERNEL_BITSERIAL) {
         if (a_layout != LOWBIT_LAYOUT_REFERENCE)
