@@ -88,6 +88,11 @@ __global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict
 }  // namespace lb
 
 namespace lb {
+size_t conv_fp4_workspace_bytes(int batch, int h, int w, int c);
+bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, int padding, long long rows);
+lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
+                              int pad, int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
+                              void* workspace, int* zero_flag, cudaStream_t stream);
 lowbit_status launch_conv_pair_im2col(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
                                       int pad, const void* weights, int b_ternary, int cout, int16_t* out,
                                       cudaStream_t stream);
@@ -145,7 +150,9 @@ extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int 
 extern "C" size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int w, int c, int kh, int kw, int stride,
                                                 int padding) {
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
-    return (size_t)rows * lowbit_plane_pitch(kh * kw * c) * (mode == LOWBIT_BNN ? 1 : 2) + 256;
+    const size_t planes = (size_t)rows * lowbit_plane_pitch(kh * kw * c) * (mode == LOWBIT_BNN ? 1 : 2) + 256;
+    const size_t fm4 = lb::conv_fp4_workspace_bytes(batch, h, w, c);  // K6's packed fp4 feature map
+    return planes > fm4 ? planes : fm4;
 }
 
 extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
@@ -162,8 +169,15 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
     // k-blocks.  BNN keeps the bit path: its padding is +-1 and a 0 activation
     // must raise ZeroInBinaryInput (conv.cpp:13, core.cpp:23).
     const bool pad_is_zero = padding == 0 || !fm_binary;
+    // K6, fp4 implicit GeMM over a packed fp4 copy of the feature map (workspace)
+    if ((kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) && workspace &&
+        lb::conv_fp4_applies(mode, fm_binary, c, cout, kh, kw, padding, rows) &&
+        (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
+        (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+        return lb::launch_conv_fp4(fm, batch, h, w, c, kh, kw, stride, padding, mode == LOWBIT_BNN && fm_binary,
+                                   weights, b_ternary, cout, out, workspace, zero_flag, (cudaStream_t)stream);
     if (mode != LOWBIT_BNN && pad_is_zero && c % 128 == 0 && rows <= 0x7FFFFFFFLL &&
-        (kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) &&
+        (kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_I8) &&
         (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0)
         return lb::launch_conv_pair_im2col(fm, batch, h, w, c, kh, kw, stride, padding, weights, b_ternary, cout, out,
                                            (cudaStream_t)stream);

@@ -90,7 +90,7 @@ def test_config4_full(lb, golden_configs):
     fm = lb.generate(0, 46, 0, 64 * 56 * 56, 128).view(64, 56, 56, 128)
     wt = lb.generate(0, 46, 1, 9 * 128, 128)
     w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(wt)))
-    for kernel in (2, 1):
+    for kernel in (2, 4, 1):  # fp4 implicit GeMM (K6), int8 implicit GeMM, K4 + bit-serial
         out = lb.conv2d_lowbit(TNN, fm, False, w, 3, 3, 1, 1, kernel=kernel)
         h = hashlib.sha256(out.cpu().numpy().astype("<i2").tobytes()).hexdigest()
         assert h == golden_configs["c4"]["sha256"], kernel
@@ -98,7 +98,8 @@ def test_config4_full(lb, golden_configs):
 
 @pytest.mark.parametrize("mode", [TNN, TBN])
 def test_conv_implicit_gemm_im2col(lb, port, mode):
-    """c % 128 == 0 and zero padding: the TMA-im2col implicit GeMM path."""
+    """c % 128 == 0 and zero padding: the TMA-im2col implicit GeMMs (0/2: fp4 K6
+    over the packed feature map, 4: int8 over the int8 map)."""
     da, db = mode_dists(mode)
     i = 0
     for (batch, h, w, ch, ksz, stride, pad) in [(2, 9, 9, 128, 3, 1, 1), (3, 8, 7, 128, 3, 2, 1), (1, 5, 5, 256, 3, 1, 0),
@@ -108,12 +109,32 @@ def test_conv_implicit_gemm_im2col(lb, port, mode):
         fm = port.generate(0, 70 + i, 0, batch * h * w, ch).reshape(batch, h, w, ch)  # ternary map -> pad 0
         wt = port.generate(db, 70 + i, 1, ksz * ksz * ch, 96)
         wts = weights_for(lb, wt, mode)
-        for kernel in (0, 2):
+        for kernel in (0, 2, 4):
             got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), False, wts, ksz, ksz, stride, pad,
                                    kernel=kernel).cpu().numpy()
             for img in range(batch):
                 want = port.direct_conv(fm[img], False, wt, ksz, ksz, stride, pad)
                 assert (got[img].astype(np.int32) == want).all(), (mode, batch, h, w, ch, ksz, stride, pad, img)
+
+
+def test_conv_fp4_binary_and_wide(lb, port):
+    """K6 on a binary map without padding (BNN, ZeroInBinaryInput still raised),
+    several n tiles (cout 400 -> 2 tiles of 208, the filter reloaded per tile)
+    and 256 channels (2 channel blocks per tap)."""
+    fm = port.generate(1, 90, 0, 2 * 7 * 7, 128).reshape(2, 7, 7, 128)
+    wt = port.generate(1, 90, 1, 9 * 128, 64)
+    got = lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, weights_for(lb, wt, BNN), 3, 3, 1, 0).cpu().numpy()
+    for img in range(2):
+        assert (got[img].astype(np.int32) == port.direct_conv(fm[img], True, wt, 3, 3, 1, 0)).all()
+    fm0 = fm.copy()
+    fm0[1, 3, 3, 5] = 0
+    with pytest.raises(lb.ZeroInBinaryInput):
+        lb.conv2d_lowbit(BNN, torch.from_numpy(fm0).cuda(), True, weights_for(lb, wt, BNN), 3, 3, 1, 0)
+    fm = port.generate(0, 91, 0, 3 * 10 * 9, 256).reshape(3, 10, 9, 256)
+    wt = port.generate(0, 91, 1, 9 * 256, 400)
+    got = lb.conv2d_lowbit(TNN, torch.from_numpy(fm).cuda(), False, weights_for(lb, wt, TNN), 3, 3, 1, 1).cpu().numpy()
+    for img in range(3):
+        assert (got[img].astype(np.int32) == port.direct_conv(fm[img], False, wt, 3, 3, 1, 1)).all()
 
 
 @pytest.mark.parametrize("mode", [BNN, TNN, TBN])
