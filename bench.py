@@ -559,13 +559,17 @@ def side_configs(lb, torch, flush, pk):
     o = torch.empty((64, 56, 56, 128), dtype=torch.int16, device="cuda")
     ops4 = 2.0 * 200704 * 128 * 1152
     res = {}
-    for kn, kid in kernels:
+    conv_paths = (("tensor_fp4", lb.KERNEL_TENSOR, fp4_peak,
+                   "K6: fm -> packed fp4 (one HBM pass) + fp4 implicit GeMM (im2col TMA, resident filter)"),
+                  ("tensor_i8", lb.KERNEL_TENSOR_I8, tensor_peak,
+                   "int8 implicit GeMM: im2col TMA over the int8 map -> tcgen05 kind::i8"),
+                  ("bitserial", lb.KERNEL_BITSERIAL, popc(1), "K4 fused im2col+encode -> K2 bit-serial"))
+    for kn, kid, peak, path in conv_paths:
         ms = time_device(torch, lambda: lb.conv2d_lowbit(1, fm, False, w, 3, 3, 1, 1, kernel=kid, out=o,
                                                          workspace=wsp), flush)
-        res[kn] = {"ms": ms, "TOPS": ops4 / (ms * 1e-3) / 1e12, "frac": ops4 / (ms * 1e-3) / 1e12 /
-                   (tensor_peak if kn == "tensor" else popc(1)),
-                   "path": ("implicit GeMM: im2col TMA -> tcgen05 (no bit planes)" if kn == "tensor"
-                            else "K4 fused im2col+encode -> K2 bit-serial")}
+        res[kn] = {"ms": ms, "TOPS": ops4 / (ms * 1e-3) / 1e12, "frac": ops4 / (ms * 1e-3) / 1e12 / peak,
+                   "path": path}
+    res["auto"] = "tensor_fp4"
     # K4 alone (HBM-bound): int8 NHWC in, two bit planes out
     pitch = lb.plane_pitch(1152)
     p0 = wsp[: 200704 * pitch]
