@@ -77,7 +77,10 @@ constexpr uint32_t F4_SF_OFF = 248;
 // all n tiles of that m tile: the converters run once per m tile instead of
 // once per (m, n) tile, and the raw planes only stream through a 16 KB ring.
 constexpr int F4_AR_SLOTS = 8;
-constexpr int F4_AR_RAW = 16 * 1024;
+#ifndef LOWBIT_F4_AR_RAW_KB
+#define LOWBIT_F4_AR_RAW_KB 16
+#endif
+constexpr int F4_AR_RAW = LOWBIT_F4_AR_RAW_KB * 1024;
 __host__ __device__ constexpr int f4_smem_bytes(bool ar) {
     return 1024 + (ar ? F4_AR_SLOTS : F4_A_ST) * F4_A_BYTES + F4_B_ST * F4_B_BYTES + (ar ? F4_AR_RAW : F4_RAW_RING) +
            4 * F4_EPI_BUFS * F4_EPI_BYTES + 1024;
