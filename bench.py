@@ -244,11 +244,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "bitserial"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "tensor_i8", "bitserial"])
     ap.add_argument("--layout", default="nibbles", choices=["nibbles", "lanes", "reference"],
                     help="A plane layout written by the (untimed) encode: nibbles -> fp4 (kind::mxf4) tensor-core "
-                         "kernel, lanes -> int8 (kind::i8) kernel, reference -> int8 kernel on the reference bit "
-                         "order")
+                         "kernel K5, lanes -> int8 (kind::i8) kernel K3, reference (the reference's own bit order) "
+                         "-> K5 for large shapes, K3 for launch-bound ones")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-config side measurements")
@@ -272,7 +272,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    kernel = {"auto": lb.KERNEL_AUTO, "tensor": lb.KERNEL_TENSOR, "bitserial": lb.KERNEL_BITSERIAL}[args.kernel]
+    kernel = {"auto": lb.KERNEL_AUTO, "tensor": lb.KERNEL_TENSOR, "tensor_i8": lb.KERNEL_TENSOR_I8,
+              "bitserial": lb.KERNEL_BITSERIAL}[args.kernel]
 
     mode, M, N, K, da, db, seed = CONFIGS[args.config]
     from paper_2205_09120_b200.shard import row_range
