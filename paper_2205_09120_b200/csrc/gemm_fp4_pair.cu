@@ -96,7 +96,9 @@ struct Fp4Params {
     int m_major;   // schedule: 1 = each pair owns whole m tiles (all n tiles back to back)
     int resident;  // raw A planes stay in the ring across the n tiles of an m tile (m_major only)
     int a_res;     // AR variant (launch selects the template; recorded for the host only)
-    int debug;  // timing experiments only (results invalid): 1 converters skip the expansion, 2 no MMAs
+    int debug;  // LOWBIT_DEBUG_FP4 timing experiments (results invalid unless only 8 is set): 1 converters
+                // skip the expansion, 2 no MMAs, 4 no epilogue, 8 role timers (valid), 16 MMA issue without
+                // waits, 64 half the B loads, 128 no TMA stores, 256 no TMEM loads, 512 no staging stores
 };
 
 // Role timing for profiling experiments (LOWBIT_DEBUG_FP4 bit 3): cycle
@@ -463,8 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * F4_EPI_BUFS * F4_EPI_BYTES;
         int acc = 0;
         uint32_t acc_phase = 0;
-        int nbuf = 0;
-        long long w_ep = 0, w_tail = 0;
+        long long w_ep = 0, w_tail = 0, w_grp[2] = {0, 0};
         const long long t_start = clock64();
         for (int i = 0; i < my_tiles; ++i) {
             int mt, nt;
@@ -491,52 +492,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             // f32 -> int16 without F2I (quarter rate): x + 1.5 * 2^23 puts the
             // integer x (|x| <= 32767) in the low mantissa bits, so its low
             // half-word IS the int16 result.
-            auto emit = [&](const uint32_t (&v)[16], int ch) {
-                uint32_t h[8];
+            auto to_i16 = [](const uint32_t (&v)[16], uint32_t (&h)[8]) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     h[j] = __byte_perm(__float_as_uint(__uint_as_float(v[2 * j]) + 12582912.0f),
                                        __float_as_uint(__uint_as_float(v[2 * j + 1]) + 12582912.0f), 0x5410);
-                const int col0 = nt * bn + ch * 16;
-                if (prm.tma_store) {
-                    const uint32_t buf = epi + (uint32_t)nbuf * F4_EPI_BYTES;
-                    if (lane == 0) bulk_wait_read<F4_EPI_BUFS - 1>();
-                    __syncwarp();
-                    const uint32_t rowaddr = buf + lane * 32;
-                    const uint32_t sw = (uint32_t)(lane >> 2) & 1;  // TMA SWIZZLE_32B
-                    sts_v4(rowaddr + (sw << 4), h[0], h[1], h[2], h[3]);
-                    sts_v4(rowaddr + ((sw ^ 1) << 4), h[4], h[5], h[6], h[7]);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_2d(&tmap_c, buf, col0, row0);
-                        bulk_commit();
-                    }
-                    nbuf = nbuf + 1 == F4_EPI_BUFS ? 0 : nbuf + 1;
-                } else {
-                    const int row = row0 + lane;
-                    if (row < prm.m) {
-                        int16_t* crow = prm.c + (long long)row * prm.ldc;
-                        if (vec_ok && col0 + 16 <= prm.n) {  // one full 32-byte sector per lane
-                            stg_v8(crow + col0, h);
-                        } else {
+            };
+            // Groups of F4_EPI_BUFS 16-column chunks: one TMEM wait, one wait for the
+            // staging buffers, one proxy fence and one bulk group per group.
+            static_assert(F4_EPI_BUFS == 4, "epilogue groups are 4 chunks");
+            long long _tg = (prm.debug & 8) ? clock64() : 0;
+            for (int g0 = 0; g0 < nch; g0 += 4) {
+                uint32_t v[4][16];
+                if (!(prm.debug & 256)) {  // debug 256: timing experiment without the TMEM loads
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (col0 + j < prm.n) crow[col0 + j] = (int16_t)(h[j >> 1] >> (16 * (j & 1)));
+                    for (int j = 0; j < 4; ++j)
+                        if (g0 + j < nch && !(tail_out && g0 + j == nch - 1))
+                            tmem_ld_32x32b_x16(tacc + (g0 + j) * 16, v[j]);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) v[j][q] = (uint32_t)(g0 + j + q);
+                }
+                if (prm.tma_store) {
+                    if (lane == 0) bulk_wait_read<0>();  // the previous group's stores have read their buffers
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int ch = g0 + j;
+                    if (ch < nch) {
+                        if (tail_out && ch == nch - 1) {
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) v[j][q] = vt[q];
+                        }
+                        uint32_t h[8];
+                        to_i16(v[j], h);
+                        const int col0 = nt * bn + ch * 16;
+                        if (prm.debug & 512) {  // timing experiment: no staging stores
+                            if ((h[0] ^ h[3] ^ h[7]) == 0x9E3779B9u && lane == 77) sts_v4(epi, h[0], h[1], h[2], h[3]);
+                        } else if (prm.tma_store) {
+                            const uint32_t rowaddr = epi + (uint32_t)j * F4_EPI_BYTES + lane * 32;
+                            const uint32_t sw = (uint32_t)(lane >> 2) & 1;  // TMA SWIZZLE_32B
+                            sts_v4(rowaddr + (sw << 4), h[0], h[1], h[2], h[3]);
+                            sts_v4(rowaddr + ((sw ^ 1) << 4), h[4], h[5], h[6], h[7]);
+                        } else {
+                            const int row = row0 + lane;
+                            if (row < prm.m) {
+                                int16_t* crow = prm.c + (long long)row * prm.ldc;
+                                if (vec_ok && col0 + 16 <= prm.n) {  // one full 32-byte sector per lane
+                                    stg_v8(crow + col0, h);
+                                } else {
+#pragma unroll
+                                    for (int q = 0; q < 16; ++q)
+                                        if (col0 + q < prm.n) crow[col0 + q] = (int16_t)(h[q >> 1] >> (16 * (q & 1)));
+                                }
+                            }
                         }
                     }
                 }
-            };
-            const int nld = tail_out ? nch - 1 : nch;
-            for (int ch = 0; ch < nld; ch += 2) {  // two TMEM loads in flight per wait
-                uint32_t va[16], vb[16];
-                tmem_ld_32x32b_x16(tacc + ch * 16, va);
-                if (ch + 1 < nld) tmem_ld_32x32b_x16(tacc + (ch + 1) * 16, vb);
-                tmem_ld_wait();
-                emit(va, ch);
-                if (ch + 1 < nld) emit(vb, ch + 1);
+                if (prm.tma_store && !(prm.debug & 128)) {  // debug 128: timing experiment without the stores
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (int j = 0; j < 4 && g0 + j < nch; ++j)
+                            tma_store_2d(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16, row0);
+                        bulk_commit();
+                    }
+                }
+                if (prm.debug & 8) {
+                    const long long now = clock64();
+                    w_grp[g0 == 0 ? 0 : 1] += now - _tg;
+                    _tg = now;
+                }
             }
-            if (tail_out) emit(vt, nch - 1);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
@@ -547,6 +578,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             atomicAdd(&g_fp4_stats[8], (unsigned long long)w_ep);
             atomicAdd(&g_fp4_stats[9], (unsigned long long)(clock64() - t_start));
             atomicAdd(&g_fp4_stats[10], (unsigned long long)w_tail);
+            atomicAdd(&g_fp4_stats[14], (unsigned long long)w_grp[0]);
+            atomicAdd(&g_fp4_stats[15], (unsigned long long)w_grp[1]);
         }
     }
 

@@ -28,4 +28,5 @@ nc = 148 * 8
 print(f"converter warp: total {v[7]/nc:.0f}, wait raw {v[4]/nc:.0f}, wait slot {v[5]/nc:.0f}, work {v[6]/nc:.0f}; "
       f"work per k-block {v[6]/nc/(kb/nl/2):.0f} cyc")
 ne = 148 * 4
-print(f"epilogue warp: total {v[9]/ne:.0f}, wait tmem_full {v[8]/ne:.0f}, tail+scales {v[10]/ne:.0f}")
+print(f"epilogue warp: total {v[9]/ne:.0f}, wait tmem_full {v[8]/ne:.0f}, tail+scales {v[10]/ne:.0f}, "
+      f"first group {v[14]/ne:.0f}, other groups {v[15]/ne:.0f}")
