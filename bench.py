@@ -594,9 +594,21 @@ def side_configs(lb, torch, flush, pk):
     ops5 = 2.0 * 1048576 * 1024 * 2048
     out["c5_from_int8"] = {"ms": ms, "TOPS": ops5 / (ms * 1e-3) / 1e12, "frac": ops5 / (ms * 1e-3) / 1e12 / tensor_peak,
                            "path": "lowbit_gemm_i8: int8 A tiles by TMA (128B swizzle) -> tcgen05 kind::i8"}
+    # the same product from the int8 sign matrix through K1 (nibble planes) + K5 (fp4): two launches
+    planes = lb.empty_planes(1048576, 2048, True)
+    planes.layout = 2
+
+    def via_planes():
+        L.check(L.lib.lowbit_encode_ex(1, 2, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,
+                                       C.c_void_p(planes.plane0.data_ptr()), C.c_void_p(planes.plane1.data_ptr()),
+                                       planes.pitch, None, st), "encode")
+        lb.gemm_lowbit(1, planes, w5, (1048576, 1024, 2048), out=c5)
+    ms = time_device(torch, via_planes, flush, reps=10)
+    out["c5_from_int8_via_fp4"] = {"ms": ms, "TOPS": ops5 / (ms * 1e-3) / 1e12,
+                                   "frac": ops5 / (ms * 1e-3) / 1e12 / fp4_peak,
+                                   "path": "K1 encode (NIBBLES planes, HBM-bound) + K5 fp4 GeMM"}
     del c5, w5
     # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
-    planes = lb.empty_planes(1048576, 2048, True)
     eb = 1048576 * 2048 + 2 * 1048576 * planes.pitch
     for lay, name in ((2, "k1_encode_c5_nibbles"), (1, "k1_encode_c5_lanes"), (0, "k1_encode_c5_reference_layout")):
         enc = lambda: L.check(L.lib.lowbit_encode_ex(1, lay, C.c_void_p(a.data_ptr()), 1048576, 2048, 2048,

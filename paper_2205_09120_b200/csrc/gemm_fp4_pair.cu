@@ -61,10 +61,10 @@ constexpr int F4_RAW_PLANE = F4_BM * 32;      // 4 KB: 128 rows x 256 bits
 constexpr int F4_RAW_RING = LOWBIT_F4_RAW_KB * 1024;
 __host__ __device__ constexpr int f4_raw_stages(bool ter) { return LOWBIT_F4_RAW_KB / (ter ? 8 : 4); }
 constexpr int F4_EPI_BYTES = 32 * 32;         // 32 rows x 16 int16, per warp per buffer
-#ifndef LOWBIT_F4_EPI_BUFS
-#define LOWBIT_F4_EPI_BUFS 4
-#endif
-constexpr int F4_EPI_BUFS = LOWBIT_F4_EPI_BUFS;  // TMA-store staging buffers per epilogue warp
+// TMA-store staging: 16 buffers of 1 KB per CTA — 4 epilogue warps x 4 (streaming
+// variant) or 8 epilogue warps x 2 (AR: its converters need one group of 4 warps
+// only, so the other 4 drain the accumulators; the epilogue is its critical path).
+constexpr int F4_EPI_TOTAL = 16;
 // Scale factors.  An fp4 MMA costs the same for any N <= 256 (measured), so
 // tiles are 256 wide, and two f32 accumulators fill all 512 TMEM columns.
 // The unit scales (SFA and SFB share one 8-column block of 0x7F bytes) live
@@ -83,7 +83,7 @@ constexpr int F4_AR_SLOTS = 8;
 constexpr int F4_AR_RAW = LOWBIT_F4_AR_RAW_KB * 1024;
 __host__ __device__ constexpr int f4_smem_bytes(bool ar) {
     return 1024 + (ar ? F4_AR_SLOTS : F4_A_ST) * F4_A_BYTES + F4_B_ST * F4_B_BYTES + (ar ? F4_AR_RAW : F4_RAW_RING) +
-           4 * F4_EPI_BUFS * F4_EPI_BYTES + 1024;
+           F4_EPI_TOTAL * F4_EPI_BYTES + 1024;
 }
 static_assert(f4_smem_bytes(false) <= 227 * 1024 && f4_smem_bytes(true) <= 227 * 1024,
               "fp4 pair kernel exceeds shared memory");
@@ -149,11 +149,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     constexpr int A_SLOTS = AR ? F4_AR_SLOTS : F4_A_ST;
+    constexpr int CONV_W = AR ? 4 : 8, EPI_W = 12 - CONV_W;  // warps 0..CONV_W-1 convert, the rest to 11 drain
+    // staging buffers (= chunks per group) per epilogue warp: 2 (4 measured equal and spills registers)
+    constexpr int EGRP = 2;
     constexpr bool SHARED = !AR && F4_SHARED_RING;  // one release barrier for the A and B slots
     uint8_t* sB = sA + A_SLOTS * F4_A_BYTES;
     uint8_t* sRaw = sB + F4_B_ST * F4_B_BYTES;
     uint8_t* sEpi = sRaw + (AR ? F4_AR_RAW : F4_RAW_RING);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * F4_EPI_BUFS * F4_EPI_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + F4_EPI_TOTAL * F4_EPI_BYTES);
     constexpr uint32_t RAW_SLOT = A_TER ? 2 * F4_RAW_PLANE : F4_RAW_PLANE;
     constexpr uint32_t RS = AR ? F4_AR_RAW / RAW_SLOT : f4_raw_stages(A_TER);
     static_assert(RS <= 16 && A_SLOTS <= 8 && F4_B_ST <= 8, "barrier table sizes");
@@ -201,12 +204,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mbar_init(&b_empty[s], 1);
         }
         for (int s = 0; s < A_SLOTS; ++s) {
-            mbar_init(&a_ready[s], 8);
+            mbar_init(&a_ready[s], AR ? 16 : 8);  // AR: one barrier per pair of k-blocks
             mbar_init(&a_empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
-            mbar_init(&tmem_empty[a], 8);
+            mbar_init(&tmem_empty[a], 2 * EPI_W);
         }
         mbar_init(&sf_ready[0], 8);
         mbar_init(&sf_ready[1], 8);
@@ -249,7 +252,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             const uint32_t pair_bytes = (uint32_t)bn * 128;
             const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
             uint32_t t = 0;
-            for (int i = 0; i < my_tiles; ++i) {
+            for (int i = 0; AR && i < my_tiles; ++i) {
+                // AR: stages of two k-blocks (one barrier per 8 MMAs: an mbarrier wait on
+                // the issuing thread stalls the MMA stream ~270 cycles)
+                int mt, nt;
+                tile_of(i, mt, nt);
+                const int brow = nt * bn + (int)rank * bnh;
+                for (int kb = 0; kb < prm.kblocks; kb += 2, ++t) {
+                    const uint32_t st = t % (F4_B_ST / 2);
+                    mbar_wait_sleep(&b_empty[st], ((t / (F4_B_ST / 2)) & 1) ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&b_full[st], 2 * pair_bytes);
+                    for (int j = 0; j < 2; ++j)
+                        tma_load_2d_pair(smem_u32(sB + (2 * st + j) * F4_B_BYTES), &tmap_b, b_full0 + st * 8,
+                                         (kb + j) * 128, brow);
+                }
+            }
+            for (int i = 0; !AR && i < my_tiles; ++i) {
                 int mt, nt;
                 tile_of(i, mt, nt);
                 const int brow = nt * bn + (int)rank * bnh;
@@ -293,12 +311,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
                 const uint32_t sf = tmem_base + (uint32_t)(acc ^ 1) * F4_MAX_BN + F4_SF_OFF;
-                for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
-                    const uint32_t sa = AR ? (uint32_t)kb : t % F4_A_ST, sb = t % F4_B_ST;
+                for (int kb = 0; AR && kb < prm.kblocks; kb += 2, t += 2) {
+                    const uint32_t t2 = t >> 1, st = t2 % (F4_B_ST / 2);
+                    if (first_nt) {  // later n tiles reuse the converted A
+                        F4_T0();
+                        mbar_wait(&a_ready[kb >> 1], mgen & 1);
+                        F4_ACC(w_a);
+                    }
+                    {
+                        F4_T0();
+                        mbar_wait(&b_full[st], (t2 / (F4_B_ST / 2)) & 1);
+                        F4_ACC(w_b);
+                    }
+                    tc_fence_after();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const uint32_t a_addr = smem_u32(sA + (kb + j) * F4_A_BYTES);
+                            const uint32_t b_addr = smem_u32(sB + (2 * st + j) * F4_B_BYTES);
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
+                                               umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf,
+                                               (kb | j | kk) != 0);
+                        }
+                        umma_commit_pair(&b_empty[st], 0x3);
+                        if (last_nt) umma_commit_pair(&a_empty[kb >> 1], 0x3);
+                    }
+                    __syncwarp();
+                }
+                for (int kb = 0; !AR && kb < prm.kblocks; ++kb, ++t) {
+                    const uint32_t sa = t % F4_A_ST, sb = t % F4_B_ST;
                     if (!(prm.debug & 16) || t < (uint32_t)F4_B_ST) {  // debug 16: MMA issue rate (no waits)
-                        if (!AR || first_nt) {  // AR: later n tiles reuse the converted A
+                        {
                             F4_T0();
-                            mbar_wait(&a_ready[sa], AR ? (mgen & 1) : (t / F4_A_ST) & 1);
+                            mbar_wait(&a_ready[sa], (t / F4_A_ST) & 1);
                             F4_ACC(w_a);
                         }
                         {
@@ -316,7 +363,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                             if (!(prm.debug & 2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                            umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf, (kb | kk) != 0);
-                        if (!AR || last_nt) umma_commit_pair(&a_empty[sa], 0x3);
+                        umma_commit_pair(&a_empty[sa], 0x3);
                         if (!SHARED) umma_commit_pair(&b_empty[sb], 0x3);
                     }
                     __syncwarp();
@@ -334,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 atomicAdd(&g_fp4_stats[12], (unsigned long long)t);
             }
         }
-    } else if (warp < 8) {
+    } else if (warp < CONV_W) {
         // ===================== converters (both CTAs) =====================
         const int g = warp >> 2;
         const int r = threadIdx.x & 127;
@@ -349,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             // one item per (m tile, k-block); kbs is even, so a group always owns
             // the same k-blocks and its waits on a slot's barriers stay in order
             const uint32_t items = (uint32_t)(my_tiles / prm.n_tiles) * kbs;
-            for (uint32_t u = g; u < items; u += 2) {
+            for (uint32_t u = g; u < items; u += CONV_W / 4) {
                 const uint32_t mgen = u / kbs, kb = u - mgen * kbs;
                 const uint32_t rs = u % RS;
                 {
@@ -372,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 if (lane == 0) mbar_arrive(&raw_empty[rs]);
                 {
                     F4_T0();
-                    mbar_wait_sleep(&a_empty[kb], (mgen & 1) ^ 1);  // last n tile of the previous m tile done
+                    mbar_wait_sleep(&a_empty[kb >> 1], (mgen & 1) ^ 1);  // last n tile of the previous m tile done
                     F4_ACC(w_slot);
                 }
                 F4_T0();
@@ -388,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 fp4_chunk<A_TER, LAYOUT>(p1.w, m1.w, row + ((7 ^ sw) << 4));
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(a_ready0 + kb * 8);
+                if (lane == 0) mbar_arrive_cluster(a_ready0 + (kb >> 1) * 8);
                 F4_ACC(w_work);
             }
         }
@@ -447,7 +494,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         }
     } else {
         // ===================== epilogue (both CTAs) =====================
-        const int wq = warp & 3;  // TMEM lane quarter
+        const int ewarp = warp - CONV_W;
+        const int wq = warp & 3;            // TMEM lane quarter (warp % 4, as tcgen05.ld/st require)
+        const int half = ewarp >> 2;        // column range of the tile this warp drains
+        constexpr int NHALF = EPI_W / 4;
+        const int nch_all = bn / 16, per_half = (nch_all + NHALF - 1) / NHALF;
+        const int ch_lo = half * per_half, ch_hi = ch_lo + per_half < nch_all ? ch_lo + per_half : nch_all;
+        // the warps draining the last chunk also own the scale hand-off (sf_ready counts 8)
+        const bool sf_owner = half == (nch_all - 1) / per_half;
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const uint32_t sf_ready0 = mapa_shared(smem_u32(&sf_ready[0]), 0);
         // unit block scales (UE8M0 0x7F = 2^0) into buffer c's tail, then tell the MMA warp
@@ -458,14 +512,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(sf_ready0 + c * 8);
         };
-        put_scales(1);  // tile 0 runs on buffer 0
+        if (sf_owner) put_scales(1);  // tile 0 runs on buffer 0
 
         const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
         const bool vec_ok = ((prm.ldc & 15) == 0) && ((reinterpret_cast<uintptr_t>(prm.c) & 31) == 0);
-        const uint32_t epi = smem_u32(sEpi) + (uint32_t)(warp - 8) * F4_EPI_BUFS * F4_EPI_BYTES;
+        const uint32_t epi = smem_u32(sEpi) + (uint32_t)ewarp * EGRP * F4_EPI_BYTES;
         int acc = 0;
         uint32_t acc_phase = 0;
-        long long w_ep = 0, w_tail = 0, w_grp[2] = {0, 0};
+        long long w_ep = 0, w_tail = 0, w_grp0 = 0, w_grp1 = 0;
         const long long t_start = clock64();
         for (int i = 0; i < my_tiles; ++i) {
             int mt, nt;
@@ -482,12 +536,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             const int nch = (prm.debug & 4) ? 0 : bn / 16;
             // tail first: the next tile's scales go there (its last chunk waits in registers)
             uint32_t vt[16];
-            const bool tail_out = bn > (int)F4_SF_OFF && nch > 0;
+            const bool tail_out = bn > (int)F4_SF_OFF && nch > 0 && sf_owner;
             if (tail_out) {
                 tmem_ld_32x32b_x16(tacc + (nch - 1) * 16, vt);
                 tmem_ld_wait();
             }
-            put_scales(acc);
+            if (sf_owner) put_scales(acc);
             F4_ACC(w_tail);
             // f32 -> int16 without F2I (quarter rate): x + 1.5 * 2^23 puts the
             // integer x (|x| <= 32767) in the low mantissa bits, so its low
@@ -498,21 +552,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     h[j] = __byte_perm(__float_as_uint(__uint_as_float(v[2 * j]) + 12582912.0f),
                                        __float_as_uint(__uint_as_float(v[2 * j + 1]) + 12582912.0f), 0x5410);
             };
-            // Groups of F4_EPI_BUFS 16-column chunks: one TMEM wait, one wait for the
+            // Groups of EGRP 16-column chunks: one TMEM wait, one wait for the
             // staging buffers, one proxy fence and one bulk group per group.
-            static_assert(F4_EPI_BUFS == 4, "epilogue groups are 4 chunks");
             long long _tg = (prm.debug & 8) ? clock64() : 0;
-            for (int g0 = 0; g0 < nch; g0 += 4) {
-                uint32_t v[4][16];
+            const int cend = nch < ch_hi ? nch : ch_hi;
+            for (int g0 = ch_lo; g0 < cend; g0 += EGRP) {
+                uint32_t v[EGRP][16];
                 if (!(prm.debug & 256)) {  // debug 256: timing experiment without the TMEM loads
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (g0 + j < nch && !(tail_out && g0 + j == nch - 1))
+                    for (int j = 0; j < EGRP; ++j)
+                        if (g0 + j < cend && !(tail_out && g0 + j == nch - 1))
                             tmem_ld_32x32b_x16(tacc + (g0 + j) * 16, v[j]);
                     tmem_ld_wait();
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < EGRP; ++j)
 #pragma unroll
                         for (int q = 0; q < 16; ++q) v[j][q] = (uint32_t)(g0 + j + q);
                 }
@@ -521,9 +575,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     __syncwarp();
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < EGRP; ++j) {
                     const int ch = g0 + j;
-                    if (ch < nch) {
+                    if (ch < cend) {
                         if (tail_out && ch == nch - 1) {
 #pragma unroll
                             for (int q = 0; q < 16; ++q) v[j][q] = vt[q];
@@ -557,14 +611,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int j = 0; j < 4 && g0 + j < nch; ++j)
+                        for (int j = 0; j < EGRP && g0 + j < cend; ++j)
                             tma_store_2d(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16, row0);
                         bulk_commit();
                     }
                 }
                 if (prm.debug & 8) {
                     const long long now = clock64();
-                    w_grp[g0 == 0 ? 0 : 1] += now - _tg;
+                    if (g0 == ch_lo) w_grp0 += now - _tg;
+                    else w_grp1 += now - _tg;
                     _tg = now;
                 }
             }
@@ -578,8 +633,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             atomicAdd(&g_fp4_stats[8], (unsigned long long)w_ep);
             atomicAdd(&g_fp4_stats[9], (unsigned long long)(clock64() - t_start));
             atomicAdd(&g_fp4_stats[10], (unsigned long long)w_tail);
-            atomicAdd(&g_fp4_stats[14], (unsigned long long)w_grp[0]);
-            atomicAdd(&g_fp4_stats[15], (unsigned long long)w_grp[1]);
+            atomicAdd(&g_fp4_stats[14], (unsigned long long)w_grp0);
+            atomicAdd(&g_fp4_stats[15], (unsigned long long)w_grp1);
         }
     }
 
