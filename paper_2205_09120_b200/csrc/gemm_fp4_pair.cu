@@ -81,9 +81,25 @@ constexpr int F4_AR_SLOTS = 8;
 #define LOWBIT_F4_AR_RAW_KB 16
 #endif
 constexpr int F4_AR_RAW = LOWBIT_F4_AR_RAW_KB * 1024;
+// AR tile width / B ring / staging (tuning knobs)
+#ifndef LOWBIT_F4_AR_BN
+#define LOWBIT_F4_AR_BN 256
+#endif
+#ifndef LOWBIT_F4_AR_B_SLOTS
+#define LOWBIT_F4_AR_B_SLOTS 4
+#endif
+#ifndef LOWBIT_F4_AR_EGRP
+#define LOWBIT_F4_AR_EGRP 2
+#endif
+constexpr int F4_AR_BN = LOWBIT_F4_AR_BN, F4_AR_B_SLOTS = LOWBIT_F4_AR_B_SLOTS, F4_AR_EGRP = LOWBIT_F4_AR_EGRP;
+constexpr int F4_AR_B_BYTES = (F4_AR_BN / 2) * 128;
+static_assert(F4_AR_B_BYTES % 1024 == 0 && F4_AR_B_SLOTS % 2 == 0, "AR B slots");
+// staging: 8 epilogue warps x F4_AR_EGRP (AR) or 4 warps x 2 buffers of 1 KB
+__host__ __device__ constexpr int f4_epi_bytes(bool ar) { return (ar ? 8 * F4_AR_EGRP : 8) * F4_EPI_BYTES; }
 __host__ __device__ constexpr int f4_smem_bytes(bool ar) {
-    return 1024 + (ar ? F4_AR_SLOTS : F4_A_ST) * F4_A_BYTES + F4_B_ST * F4_B_BYTES + (ar ? F4_AR_RAW : F4_RAW_RING) +
-           F4_EPI_TOTAL * F4_EPI_BYTES + 1024;
+    return 1024 + (ar ? F4_AR_SLOTS : F4_A_ST) * F4_A_BYTES +
+           (ar ? F4_AR_B_SLOTS * F4_AR_B_BYTES : F4_B_ST * F4_B_BYTES) + (ar ? F4_AR_RAW : F4_RAW_RING) +
+           f4_epi_bytes(ar) + 1024;
 }
 static_assert(f4_smem_bytes(false) <= 227 * 1024 && f4_smem_bytes(true) <= 227 * 1024,
               "fp4 pair kernel exceeds shared memory");
@@ -151,15 +167,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
     constexpr int A_SLOTS = AR ? F4_AR_SLOTS : F4_A_ST;
     constexpr int CONV_W = AR ? 4 : 8, EPI_W = 12 - CONV_W;  // warps 0..CONV_W-1 convert, the rest to 11 drain
     // staging buffers (= chunks per group) per epilogue warp: 2 (4 measured equal and spills registers)
-    constexpr int EGRP = 2;
+    constexpr int EGRP = AR ? F4_AR_EGRP : 2;
+    constexpr int B_SLOTS = AR ? F4_AR_B_SLOTS : F4_B_ST, B_BYTES = AR ? F4_AR_B_BYTES : F4_B_BYTES;
     constexpr bool SHARED = !AR && F4_SHARED_RING;  // one release barrier for the A and B slots
     uint8_t* sB = sA + A_SLOTS * F4_A_BYTES;
-    uint8_t* sRaw = sB + F4_B_ST * F4_B_BYTES;
+    uint8_t* sRaw = sB + B_SLOTS * B_BYTES;
     uint8_t* sEpi = sRaw + (AR ? F4_AR_RAW : F4_RAW_RING);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + F4_EPI_TOTAL * F4_EPI_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + f4_epi_bytes(AR));
     constexpr uint32_t RAW_SLOT = A_TER ? 2 * F4_RAW_PLANE : F4_RAW_PLANE;
     constexpr uint32_t RS = AR ? F4_AR_RAW / RAW_SLOT : f4_raw_stages(A_TER);
-    static_assert(RS <= 16 && A_SLOTS <= 8 && F4_B_ST <= 8, "barrier table sizes");
+    static_assert(RS <= 16 && A_SLOTS <= 8 && B_SLOTS <= 8, "barrier table sizes");
     uint64_t* raw_full = bars;                       // local: raw planes landed            [raw]
     uint64_t* raw_empty = bars + 16;                 // local: 4 converter warps read them  [raw]
     uint64_t* b_full = bars + 32;                    // leader: both halves of B landed     [b]
@@ -199,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mbar_init(&raw_full[s], 1);
             mbar_init(&raw_empty[s], 4);
         }
-        for (int s = 0; s < F4_B_ST; ++s) {
+        for (int s = 0; s < B_SLOTS; ++s) {
             mbar_init(&b_full[s], 1);
             mbar_init(&b_empty[s], 1);
         }
@@ -259,11 +276,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 tile_of(i, mt, nt);
                 const int brow = nt * bn + (int)rank * bnh;
                 for (int kb = 0; kb < prm.kblocks; kb += 2, ++t) {
-                    const uint32_t st = t % (F4_B_ST / 2);
-                    mbar_wait_sleep(&b_empty[st], ((t / (F4_B_ST / 2)) & 1) ^ 1);
+                    const uint32_t st = t % (B_SLOTS / 2);
+                    mbar_wait_sleep(&b_empty[st], ((t / (B_SLOTS / 2)) & 1) ^ 1);
                     if (leader) mbar_arrive_expect_tx(&b_full[st], 2 * pair_bytes);
                     for (int j = 0; j < 2; ++j)
-                        tma_load_2d_pair(smem_u32(sB + (2 * st + j) * F4_B_BYTES), &tmap_b, b_full0 + st * 8,
+                        tma_load_2d_pair(smem_u32(sB + (2 * st + j) * B_BYTES), &tmap_b, b_full0 + st * 8,
                                          (kb + j) * 128, brow);
                 }
             }
@@ -312,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * F4_MAX_BN;
                 const uint32_t sf = tmem_base + (uint32_t)(acc ^ 1) * F4_MAX_BN + F4_SF_OFF;
                 for (int kb = 0; AR && kb < prm.kblocks; kb += 2, t += 2) {
-                    const uint32_t t2 = t >> 1, st = t2 % (F4_B_ST / 2);
+                    const uint32_t t2 = t >> 1, st = t2 % (B_SLOTS / 2);
                     if (first_nt) {  // later n tiles reuse the converted A
                         F4_T0();
                         mbar_wait(&a_ready[kb >> 1], mgen & 1);
@@ -320,7 +337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     }
                     {
                         F4_T0();
-                        mbar_wait(&b_full[st], (t2 / (F4_B_ST / 2)) & 1);
+                        mbar_wait(&b_full[st], (t2 / (B_SLOTS / 2)) & 1);
                         F4_ACC(w_b);
                     }
                     tc_fence_after();
@@ -328,7 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
                             const uint32_t a_addr = smem_u32(sA + (kb + j) * F4_A_BYTES);
-                            const uint32_t b_addr = smem_u32(sB + (2 * st + j) * F4_B_BYTES);
+                            const uint32_t b_addr = smem_u32(sB + (2 * st + j) * B_BYTES);
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)
                                 umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
@@ -660,8 +677,8 @@ namespace lb {
 
 // BN: the fewest column tiles of <= 256 (an MMA costs the same for any N <= 256),
 // then the smallest multiple of 16 covering n (less B traffic).
-static int pick_bn_fp4(int n) {
-    const int tiles = (n + F4_MAX_BN - 1) / F4_MAX_BN;
+static int pick_bn_fp4(int n, int max_bn = F4_MAX_BN) {
+    const int tiles = (n + max_bn - 1) / max_bn;
     const int per = (n + tiles - 1) / tiles;
     return (per + 15) / 16 * 16;
 }
@@ -712,7 +729,11 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
         return e ? atoi(e) : 0;
     }();
     prm.a_res = !no_ar && prm.m_major && prm.n_tiles >= 2 && prm.kblocks <= F4_AR_SLOTS && prm.kblocks % 2 == 0;
-    if (prm.a_res) prm.resident = 1;  // raw planes load once per m tile
+    if (prm.a_res) {
+        prm.resident = 1;  // raw planes load once per m tile
+        prm.bn = pick_bn_fp4(n, F4_AR_BN);
+        prm.n_tiles = (n + prm.bn - 1) / prm.bn;
+    }
     static const int debug = [] {
         const char* e = getenv("LOWBIT_DEBUG_FP4");
         return e ? atoi(e) : 0;
