@@ -210,6 +210,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         }
     };
     const int bn = prm.bn, bnh = prm.bn >> 1;
+    // streaming variant: the 4-slot shared ring runs as 2 stages of 2 k-blocks when the
+    // tile's k-block count is even (one barrier wait per 8 MMAs on the issuing thread)
+    const bool g2 = !AR && SHARED && F4_A_ST == 4 && (prm.kblocks % 2 == 0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < (int)RS; ++s) {
@@ -221,7 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mbar_init(&b_empty[s], 1);
         }
         for (int s = 0; s < A_SLOTS; ++s) {
-            mbar_init(&a_ready[s], AR ? 16 : 8);  // AR: one barrier per pair of k-blocks
+            mbar_init(&a_ready[s], (AR || g2) ? 16 : 8);  // one barrier per pair of k-blocks
             mbar_init(&a_empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -284,7 +287,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                                          (kb + j) * 128, brow);
                 }
             }
-            for (int i = 0; !AR && i < my_tiles; ++i) {
+            for (int i = 0; g2 && i < my_tiles; ++i) {
+                int mt, nt;
+                tile_of(i, mt, nt);
+                const int brow = nt * bn + (int)rank * bnh;
+                for (int kb = 0; kb < prm.kblocks; kb += 2, t += 2) {
+                    const uint32_t st = (t >> 1) & 1;
+                    mbar_wait_sleep(&a_empty[st], ((t >> 2) & 1) ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&b_full[st], 2 * pair_bytes);
+                    for (int j = 0; j < 2; ++j)
+                        tma_load_2d_pair(smem_u32(sB + (2 * st + j) * F4_B_BYTES), &tmap_b, b_full0 + st * 8,
+                                         (kb + j) * 128, brow);
+                }
+            }
+            for (int i = 0; !AR && !g2 && i < my_tiles; ++i) {
                 int mt, nt;
                 tile_of(i, mt, nt);
                 const int brow = nt * bn + (int)rank * bnh;
@@ -357,7 +373,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     }
                     __syncwarp();
                 }
-                for (int kb = 0; !AR && kb < prm.kblocks; ++kb, ++t) {
+                for (int kb = 0; g2 && kb < prm.kblocks; kb += 2, t += 2) {
+                    const uint32_t st = (t >> 1) & 1, ph = (t >> 2) & 1;
+                    {
+                        F4_T0();
+                        mbar_wait(&a_ready[st], ph);
+                        F4_ACC(w_a);
+                    }
+                    {
+                        F4_T0();
+                        mbar_wait(&b_full[st], ph);
+                        F4_ACC(w_b);
+                    }
+                    tc_fence_after();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const uint32_t a_addr = smem_u32(sA + (2 * st + j) * F4_A_BYTES);
+                            const uint32_t b_addr = smem_u32(sB + (2 * st + j) * F4_B_BYTES);
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
+                                               umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf,
+                                               (kb | j | kk) != 0);
+                        }
+                        umma_commit_pair(&a_empty[st], 0x3);  // releases both slots of the stage (A and B)
+                    }
+                    __syncwarp();
+                }
+                for (int kb = 0; !AR && !g2 && kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t sa = t % F4_A_ST, sb = t % F4_B_ST;
                     if (!(prm.debug & 16) || t < (uint32_t)F4_B_ST) {  // debug 16: MMA issue rate (no waits)
                         {
@@ -463,6 +507,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             const uint32_t u = prm.resident ? (seq / nts) * kbs + kb : t;
             const bool release = !prm.resident || nt == nts - 1;
             const uint32_t rs = u % RS, st = t % F4_A_ST;
+            // g2: slot st belongs to stage (t/2)%2, released and signalled per stage
+            const uint32_t bar_i = g2 ? (t >> 1) & 1 : st, bar_ph = g2 ? (t >> 2) & 1 : (t / F4_A_ST) & 1;
             {
                 F4_T0();
                 mbar_wait_sleep(&raw_full[rs], (u / RS) & 1);
@@ -470,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             }
             {
                 F4_T0();
-                mbar_wait_sleep(&a_empty[st], ((t / F4_A_ST) & 1) ^ 1);
+                mbar_wait_sleep(&a_empty[bar_i], bar_ph ^ 1);
                 F4_ACC(w_slot);
             }
             F4_T0();
@@ -499,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             __syncwarp();
             if (lane == 0) {
                 if (release) mbar_arrive(&raw_empty[rs]);
-                mbar_arrive_cluster(a_ready0 + st * 8);
+                mbar_arrive_cluster(a_ready0 + bar_i * 8);
             }
             F4_ACC(w_work);
         }
