@@ -253,6 +253,17 @@ LB_DEV void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t lead
         "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
         : "memory");
 }
+// Pair-form TMA load multicast to the CTAs in cta_mask (same shared offset in
+// each); the completion bytes land on each destination's pair-leader barrier
+// (mbar: this CTA's barrier address with the peer bit cleared).
+LB_DEV void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, uint32_t mbar_leader_form, int x, int y,
+                                uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_leader_form), "r"(x), "r"(y), "h"(cta_mask)
+        : "memory");
+}
 // im2col-mode TMA (pair form): 4-D NHWC map {c, w, h, n} + filter-tap offsets.
 LB_DEV void tma_load_im2col_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c, int w, int h,
                                     int n, uint16_t off_w, uint16_t off_h) {

@@ -106,6 +106,7 @@ static_assert(f4_smem_bytes(false) <= 227 * 1024 && f4_smem_bytes(true) <= 227 *
 
 struct Fp4Params {
     int m, n, kblocks, bn, m_tiles, n_tiles;
+    int m_off;  // first m tile of this launch (a split launch runs the rest elsewhere)
     long long ldc;
     int16_t* c;
     int tma_store;
@@ -156,8 +157,12 @@ __device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) 
     sts_v4(dst, o[0], o[1], o[2], o[3]);
 }
 
-template <bool A_TER, bool AR, int LAYOUT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
+// CL = 4 (AR only): two CTA pairs per cluster run different m tiles over the same
+// n tiles in lockstep and share B: each CTA loads one k-block half of a B stage
+// and multicasts it to the same-position CTA of the other pair, halving B's
+// L2 -> SM traffic.
+template <bool A_TER, bool AR, int LAYOUT, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
     gemm_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
                          const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_c,
                          const Fp4Params prm) {
@@ -190,17 +195,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
+    static_assert(CL == 2 || (CL == 4 && AR), "4-CTA clusters for the A-resident variant only");
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1;            // position in the CTA pair
+    const uint32_t pbase = crank & ~1u;         // cluster rank of this pair's leader
     const bool leader = rank == 0;
+    const uint16_t pair_mask = (uint16_t)(0x3u << pbase);
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int clu = blockIdx.x >> 2, nclu = gridDim.x >> 2, pc = (blockIdx.x >> 1) & 1;  // CL = 4
     // Schedule.  m_major: pair p owns m tiles p, p + npairs, ... and runs every
     // n tile of one m tile back to back (so its A rows can stay resident);
     // otherwise (fewer m tiles than pairs) tiles are dealt round-robin.
     const int num_tiles = prm.m_tiles * prm.n_tiles;
-    const int my_tiles = prm.m_major ? (prm.m_tiles > pair ? (prm.m_tiles - pair + npairs - 1) / npairs : 0) * prm.n_tiles
-                                     : (num_tiles > pair ? (num_tiles - pair + npairs - 1) / npairs : 0);
+    const int m_pairs = (prm.m_tiles + 1) / 2;  // CL = 4: cluster c owns m-tile pairs c, c + nclu, ...
+    const int my_tiles =
+        CL == 4 ? (m_pairs > clu ? (m_pairs - clu + nclu - 1) / nclu : 0) * prm.n_tiles
+        : prm.m_major ? (prm.m_tiles > pair ? (prm.m_tiles - pair + npairs - 1) / npairs : 0) * prm.n_tiles
+                      : (num_tiles > pair ? (num_tiles - pair + npairs - 1) / npairs : 0);
     auto tile_of = [&](int i, int& mt, int& nt) {
-        if (prm.m_major) {
+        if (CL == 4) {  // m tile 2q + pc may be past the end (rows >= m: zero A, clipped stores)
+            mt = 2 * (clu + (i / prm.n_tiles) * nclu) + pc;
+            nt = i % prm.n_tiles;
+        } else if (prm.m_major) {
             mt = pair + (i / prm.n_tiles) * npairs;
             nt = i % prm.n_tiles;
         } else {
@@ -208,6 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
             mt = tile / prm.n_tiles;
             nt = tile - mt * prm.n_tiles;
         }
+        mt += prm.m_off;
     };
     const int bn = prm.bn, bnh = prm.bn >> 1;
     // streaming variant: the 4-slot shared ring runs as 2 stages of 2 k-blocks when the
@@ -221,7 +238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         }
         for (int s = 0; s < B_SLOTS; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], 1);
+            mbar_init(&b_empty[s], CL == 4 ? 2 : 1);  // CL = 4: released by both pairs' MMAs
         }
         for (int s = 0; s < A_SLOTS; ++s) {
             mbar_init(&a_ready[s], (AR || g2) ? 16 : 8);  // one barrier per pair of k-blocks
@@ -270,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         // ===================== B producer (both CTAs; bytes land on the leader) =====================
         if (lane == 0) {
             const uint32_t pair_bytes = (uint32_t)bn * 128;
-            const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
+            const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), pbase);
             uint32_t t = 0;
             for (int i = 0; AR && i < my_tiles; ++i) {
                 // AR: stages of two k-blocks (one barrier per 8 MMAs: an mbarrier wait on
@@ -282,6 +299,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     const uint32_t st = t % (B_SLOTS / 2);
                     mbar_wait_sleep(&b_empty[st], ((t / (B_SLOTS / 2)) & 1) ^ 1);
                     if (leader) mbar_arrive_expect_tx(&b_full[st], 2 * pair_bytes);
+                    if (CL == 4) {  // k-block pc of the stage, this CTA's half, to both pairs
+                        tma_load_2d_pair_mc(smem_u32(sB + (2 * st + pc) * B_BYTES), &tmap_b,
+                                            smem_u32(&b_full[st]) & 0xFEFFFFFFu, (kb + pc) * 128, brow,
+                                            (uint16_t)((1u << rank) | (1u << (rank + 2))));
+                        continue;
+                    }
                     for (int j = 0; j < 2; ++j)
                         tma_load_2d_pair(smem_u32(sB + (2 * st + j) * B_BYTES), &tmap_b, b_full0 + st * 8,
                                          (kb + j) * 128, brow);
@@ -368,8 +391,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                                                umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf,
                                                (kb | j | kk) != 0);
                         }
-                        umma_commit_pair(&b_empty[st], 0x3);
-                        if (last_nt) umma_commit_pair(&a_empty[kb >> 1], 0x3);
+                        // CL = 4: both pairs' CTAs hold copies of this B stage (multicast)
+                        umma_commit_pair(&b_empty[st], CL == 4 ? (uint16_t)0xF : pair_mask);
+                        if (last_nt) umma_commit_pair(&a_empty[kb >> 1], pair_mask);
                     }
                     __syncwarp();
                 }
@@ -397,7 +421,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                                                umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf,
                                                (kb | j | kk) != 0);
                         }
-                        umma_commit_pair(&a_empty[st], 0x3);  // releases both slots of the stage (A and B)
+                        umma_commit_pair(&a_empty[st], pair_mask);  // releases both slots of the stage (A and B)
                     }
                     __syncwarp();
                 }
@@ -424,12 +448,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
                             if (!(prm.debug & 2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                            umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf, (kb | kk) != 0);
-                        umma_commit_pair(&a_empty[sa], 0x3);
-                        if (!SHARED) umma_commit_pair(&b_empty[sb], 0x3);
+                        umma_commit_pair(&a_empty[sa], pair_mask);
+                        if (!SHARED) umma_commit_pair(&b_empty[sb], pair_mask);
                     }
                     __syncwarp();
                 }
-                if (lane == 0) umma_commit_pair(&tmem_full[acc], 0x3);
+                if (lane == 0) umma_commit_pair(&tmem_full[acc], pair_mask);
                 __syncwarp();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
@@ -447,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         const int g = warp >> 2;
         const int r = threadIdx.x & 127;
         const uint32_t sA_u = smem_u32(sA), sRaw_u = smem_u32(sRaw);
-        const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), 0);
+        const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), pbase);
         const uint32_t kbs = (uint32_t)prm.kblocks, nts = (uint32_t)prm.n_tiles;
         const uint32_t total = (uint32_t)my_tiles * kbs;
         const uint32_t rsw = (uint32_t)(r >> 2) & 1;  // TMA SWIZZLE_32B on the raw rows
@@ -566,7 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         // the warps draining the last chunk also own the scale hand-off (sf_ready counts 8)
         const bool sf_owner = half == (nch_all - 1) / per_half;
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const uint32_t sf_ready0 = mapa_shared(smem_u32(&sf_ready[0]), 0);
+        const uint32_t sf_ready0 = mapa_shared(smem_u32(&sf_ready[0]), pbase);
         // unit block scales (UE8M0 0x7F = 2^0) into buffer c's tail, then tell the MMA warp
         auto put_scales = [&](int c) {
             tmem_st_32x32b_x8_fill(tmem_base + lane_base + (uint32_t)c * F4_MAX_BN + F4_SF_OFF, 0x7F7F7F7Fu);
@@ -577,7 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F4_THREADS, 1)
         };
         if (sf_owner) put_scales(1);  // tile 0 runs on buffer 0
 
-        const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
+        const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), pbase);
         const bool vec_ok = ((prm.ldc & 15) == 0) && ((reinterpret_cast<uintptr_t>(prm.c) & 31) == 0);
         const uint32_t epi = smem_u32(sEpi) + (uint32_t)ewarp * EGRP * F4_EPI_BYTES;
         int acc = 0;
@@ -729,17 +753,35 @@ static int pick_bn_fp4(int n, int max_bn = F4_MAX_BN) {
     return (per + 15) / 16 * 16;
 }
 
-template <bool A_TER, bool AR, int LAYOUT>
+template <bool A_TER, bool AR, int LAYOUT, int CL = 2>
 static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                         const CUtensorMap& mc, const Fp4Params& prm, int pairs, cudaStream_t stream) {
     static bool attr = false;
+    static int max_clusters = 0;
     constexpr int smem = f4_smem_bytes(AR);
+    auto kern = gemm_fp4_pair_kernel<A_TER, AR, LAYOUT, CL>;
     if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_pair_kernel<A_TER, AR, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem));
+        LB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (CL == 4) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(4 * 37);
+            cfg.blockDim = dim3(F4_THREADS);
+            cfg.dynamicSmemBytes = smem;
+            LB_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+        }
         attr = true;
     }
-    gemm_fp4_pair_kernel<A_TER, AR, LAYOUT><<<2 * pairs, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
+    int grid = 2 * pairs;
+    if (CL == 4) {  // whole clusters, all co-resident (a later wave would serialise the lockstep pairs)
+        int clusters = (prm.m_tiles + 1) / 2 < pairs / 2 ? (prm.m_tiles + 1) / 2 : pairs / 2;
+        if (max_clusters > 0 && clusters > max_clusters) clusters = max_clusters;
+        grid = 4 * (clusters > 0 ? clusters : 1);
+    }
+    static const bool verbose = getenv("LOWBIT_FP4_VERBOSE") != nullptr;
+    if (verbose)
+        std::fprintf(stderr, "fp4 kernel: AR %d layout %d CL %d grid %d (max clusters %d) bn %d n_tiles %d m_tiles %d\n",
+                     (int)AR, LAYOUT, CL, grid, max_clusters, prm.bn, prm.n_tiles, prm.m_tiles);
+    kern<<<grid, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }
@@ -810,6 +852,21 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
     const int work = prm.m_major ? prm.m_tiles : prm.m_tiles * prm.n_tiles;
     const int pairs = work < num_sms() / 2 ? work : num_sms() / 2;
 #define F4_LAUNCH(TER, AR_, LAY) launch_fp4_variant<TER, AR_, LAY>(mb, ma0, ma1, mc, prm, pairs, stream)
+    static const int cl4 = [] {
+        const char* e = getenv("LOWBIT_FP4_CL4");  // 4-CTA clusters with multicast B for the AR variant
+        return e ? atoi(e) : 0;
+    }();
+    if (prm.a_res && cl4) {
+        // Tuning experiment (LOWBIT_FP4_CL4=1): multicast B across 4-CTA clusters.  Per SM the
+        // k-block time drops ~8% (half the B traffic), but only 33 clusters (132 SMs) fit the
+        // GPCs, so it measured 3% slower on c5 (and ~0.5% faster when the leftover TPCs ran a
+        // concurrent pair kernel on the remaining m tiles).
+        return layout == LOWBIT_LAYOUT_NIBBLES
+                   ? (a_ternary ? launch_fp4_variant<true, true, 2, 4>(mb, ma0, ma1, mc, prm, pairs, stream)
+                                : launch_fp4_variant<false, true, 2, 4>(mb, ma0, ma1, mc, prm, pairs, stream))
+                   : (a_ternary ? launch_fp4_variant<true, true, 0, 4>(mb, ma0, ma1, mc, prm, pairs, stream)
+                                : launch_fp4_variant<false, true, 0, 4>(mb, ma0, ma1, mc, prm, pairs, stream));
+    }
     if (layout == LOWBIT_LAYOUT_NIBBLES) {
         if (prm.a_res) return a_ternary ? F4_LAUNCH(true, true, 2) : F4_LAUNCH(false, true, 2);
         return a_ternary ? F4_LAUNCH(true, false, 2) : F4_LAUNCH(false, false, 2);

@@ -160,3 +160,28 @@ def test_config3_fp4_hash(lb, golden_configs):
     w = lb.prepare_weights(lb.pack_b(lb.encode_binary(lb.generate(1, 45, 1, k, n))))
     c = lb.gemm_lowbit(BNN, ap, w, (m, n, k), kernel=2)
     assert sha(host(c)) == golden_configs["c3"]["sha256"]
+
+
+def test_gemm_fp4_cluster4_multicast_experiment(lb):
+    """The 4-CTA-cluster variant with multicast B (a tuning experiment behind
+    LOWBIT_FP4_CL4=1, read once per process) stays bit-exact."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, torch, paper_2205_09120_b200 as lb\n"
+        "from oracle.oracle import Port\n"
+        "p = Port()\n"
+        "for mode, (m, n, k) in [(1, (40000, 520, 2048)), (0, (19000, 300, 1024)), (2, (25000, 1024, 512))]:\n"
+        "    da, db = {0: (1, 1), 1: (0, 0), 2: (2, 1)}[mode]\n"
+        "    a = p.generate(da, 9, 0, m, k); b = p.generate(db, 9, 1, k, n)\n"
+        "    at = torch.from_numpy(a).cuda()\n"
+        "    ap = lb.encode_binary(at, layout=2) if mode == 0 else lb.encode_ternary(at, layout=2)\n"
+        "    bp = lb.encode_ternary(torch.from_numpy(b).cuda()) if mode == 1 else lb.encode_binary(torch.from_numpy(b).cuda())\n"
+        "    got = lb.gemm_lowbit(mode, ap, lb.prepare_weights(lb.pack_b(bp)), (m, n, k), kernel=2).cpu().numpy()\n"
+        "    assert (got == p.gemm(mode, a, b)).all(), (mode, m, n, k)\n"
+        "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root,
+                       env=dict(os.environ, LOWBIT_FP4_CL4="1"))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
