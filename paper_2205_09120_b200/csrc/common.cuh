@@ -264,6 +264,14 @@ LB_DEV void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, uint32_t m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_leader_form), "r"(x), "r"(y), "h"(cta_mask)
         : "memory");
 }
+// 3-D tiled TMA load whose completion bytes land on the LEADER CTA's mbarrier (pair mode).
+LB_DEV void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+        "%5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
 // im2col-mode TMA (pair form): 4-D NHWC map {c, w, h, n} + filter-tap offsets.
 LB_DEV void tma_load_im2col_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c, int w, int h,
                                     int n, uint16_t off_w, uint16_t off_h) {

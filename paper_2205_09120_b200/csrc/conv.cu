@@ -89,7 +89,8 @@ __global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict
 
 namespace lb {
 size_t conv_fp4_workspace_bytes(int batch, int h, int w, int c);
-bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, int padding, long long rows);
+bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, int padding, long long rows,
+                      int stride);
 lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
                               int pad, int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
                               void* workspace, int* zero_flag, cudaStream_t stream);
@@ -171,7 +172,7 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
     const bool pad_is_zero = padding == 0 || !fm_binary;
     // K6, fp4 implicit GeMM over a packed fp4 copy of the feature map (workspace)
     if ((kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) && workspace &&
-        lb::conv_fp4_applies(mode, fm_binary, c, cout, kh, kw, padding, rows) &&
+        lb::conv_fp4_applies(mode, fm_binary, c, cout, kh, kw, padding, rows, stride) &&
         (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
         (reinterpret_cast<uintptr_t>(out) & 15) == 0)
         return lb::launch_conv_fp4(fm, batch, h, w, c, kh, kw, stride, padding, mode == LOWBIT_BNN && fm_binary,

@@ -67,13 +67,22 @@ LB_DEV uint64_t umma_desc_k_sw64(uint32_t smem_addr) {
     return d;
 }
 
+// PT ("tap pair", 3-wide filters, stride 1, padding 1, c = 128): a k-block is two
+// horizontally adjacent taps = one 128-byte virtual pixel of the padded fm4 map
+// (make_map_im2col_pairtap): (zero dummy, tap (ky,0)) and (tap (ky,1), tap (ky,2)),
+// the filter side read straight from the prepared weights by a 3-D map whose
+// out-of-bounds half row is zero-filled (make_map_filter_pairtap).  6 loads of
+// 128-byte rows replace 9 of 64 bytes per output tile (the im2col TMA's cost
+// is per pixel row).
+template <bool PT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
     conv_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_c, const ConvF4Params prm) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int A_ST = prm.a_st;
-    const int a_stage = prm.g * C6_KB_BYTES;
+    constexpr int KB_BYTES = PT ? 2 * C6_KB_BYTES : C6_KB_BYTES;  // one k-block of A (128 or 64-byte rows)
+    const int a_stage = prm.g * KB_BYTES;
     uint8_t* sB = smem;                                  // resident filter: kblocks x breg
     uint8_t* sA = sB + prm.kblocks * prm.breg;           // A ring: A_ST x g k-blocks (1 KB multiples)
     uint8_t* sEpi = smem + C6_RING_BUDGET;
@@ -136,12 +145,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                     for (int sg = 0; sg < stages_per_tile; ++sg, ++t) {
                         const uint32_t s = t % A_ST;
                         mbar_wait_sleep(&a_empty[s], ((t / A_ST) & 1) ^ 1);
-                        if (leader) mbar_arrive_expect_tx(&a_full[s], 2u * G * C6_KB_BYTES);
+                        if (leader) mbar_arrive_expect_tx(&a_full[s], 2u * G * KB_BYTES);
                         for (int j = 0; j < G; ++j) {
                             const int kb = sg * G + j;
-                            const int tap = kb / prm.cblocks, cb = kb - tap * prm.cblocks;
-                            const int ky = tap / prm.kw, kx = tap - ky * prm.kw;
-                            tma_load_im2col_4d_pair(smem_u32(sA + s * a_stage + j * C6_KB_BYTES), &tmap_a,
+                            int cb, ky, kx;
+                            if (PT) {  // k-block 2*ky + g: (dummy, tap (ky,0)) at offset 0, taps (ky,1),(ky,2) at 2
+                                cb = 0;
+                                ky = kb >> 1;
+                                kx = 2 * (kb & 1);
+                            } else {
+                                const int tap = kb / prm.cblocks;
+                                cb = kb - tap * prm.cblocks;
+                                ky = tap / prm.kw;
+                                kx = tap - ky * prm.kw;
+                            }
+                            tma_load_im2col_4d_pair(smem_u32(sA + s * a_stage + j * KB_BYTES), &tmap_a,
                                                     a_full0 + s * 8, cb * 64, ox * prm.stride - prm.pad,
                                                     oy * prm.stride - prm.pad, img, (uint16_t)kx, (uint16_t)ky);
                         }
@@ -155,10 +173,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
             for (int nt = 0; nt < prm.n_tiles; ++nt) {
                 if (my_m == 0) break;
                 mbar_wait_sleep(b_empty, (nt & 1) ^ 1);
-                if (leader) mbar_arrive_expect_tx(b_full, (uint32_t)prm.kblocks * bn * 64);
+                if (leader) mbar_arrive_expect_tx(b_full, (uint32_t)prm.kblocks * bn * (PT ? 128 : 64));
                 const int brow = nt * bn + (int)rank * bnh;
-                for (int kb = 0; kb < prm.kblocks; ++kb)
-                    tma_load_2d_pair(smem_u32(sB + kb * prm.breg), &tmap_b, b_full0, kb * 64, brow);
+                for (int kb = 0; kb < prm.kblocks; ++kb) {
+                    if (PT)  // (zero, tap (ky,0)) at byte -64, (tap (ky,1), tap (ky,2)) at byte 64
+                        tma_load_3d_pair(smem_u32(sB + kb * prm.breg), &tmap_b, b_full0, (kb & 1) ? 64 : -64, kb >> 1,
+                                         brow);
+                    else
+                        tma_load_2d_pair(smem_u32(sB + kb * prm.breg), &tmap_b, b_full0, kb * 64, brow);
+                }
             }
         }
     } else if (warp == C6_W_MMA) {
@@ -185,12 +208,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                         if (lane == 0) {
                             for (int j = 0; j < G; ++j) {
                                 const int kb = sg * G + j;
-                                const uint32_t a_addr = smem_u32(sA + s * a_stage + j * C6_KB_BYTES);
+                                const uint32_t a_addr = smem_u32(sA + s * a_stage + j * KB_BYTES);
                                 const uint32_t b_addr = smem_u32(sB + kb * prm.breg);
 #pragma unroll
-                                for (int h = 0; h < 2; ++h)  // K = 64 per MMA = 32 bytes of the 64-byte rows
-                                    umma_mxf4_pair(d_tmem, umma_desc_k_sw64(a_addr + h * 32),
-                                                   umma_desc_k_sw64(b_addr + h * 32), idesc, sf, sf, (kb | h) != 0);
+                                for (int h = 0; h < (PT ? 4 : 2); ++h)  // K = 64 per MMA = 32 bytes of the row
+                                    umma_mxf4_pair(d_tmem,
+                                                   PT ? umma_desc_k_sw128(a_addr + h * 32) : umma_desc_k_sw64(a_addr + h * 32),
+                                                   PT ? umma_desc_k_sw128(b_addr + h * 32) : umma_desc_k_sw64(b_addr + h * 32),
+                                                   idesc, sf, sf, (kb | h) != 0);
                             }
                             umma_commit_pair(&a_empty[s], 0x3);
                         }
@@ -271,8 +296,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
 // fm int8 NHWC -> packed e2m1 (two channels per byte, channel 2i in the low
 // nibble).  One thread per 32 channels.  A 0 in a binary feature map sets
 // *zero_flag (core.cpp:23).
+// pad_w > 0: the output rows carry one extra zero pixel (row pitch pad_w + 1
+// pixels, pad_w = the map's width) for the tap-pair map.
 __global__ void conv_pack_fp4_kernel(const int8_t* __restrict__ fm, long long groups, int check_zero,
-                                     uint8_t* __restrict__ out, int* __restrict__ zero_flag) {
+                                     uint8_t* __restrict__ out, int* __restrict__ zero_flag, int pad_w, int gpp) {
     for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
          gi += (long long)gridDim.x * blockDim.x) {
         const uint4 lo = __ldg(reinterpret_cast<const uint4*>(fm) + 2 * gi);
@@ -297,7 +324,16 @@ __global__ void conv_pack_fp4_kernel(const int8_t* __restrict__ fm, long long gr
             o[q] = half[0] | (half[1] << 16);
         }
         const bool zero = check_zero && nz_all != 0x01010101u;
-        reinterpret_cast<uint4*>(out)[gi] = make_uint4(o[0], o[1], o[2], o[3]);
+        long long oi = gi;
+        if (pad_w > 0) {  // group gi = (pixel, channel group); pixel = row * pad_w + x (32-bit: < 2^31 groups)
+            // rows of pad_w + 1 pixels, a zero pixel first; one more zero pixel after the last row
+            const uint32_t g32 = (uint32_t)gi, pix = g32 / (uint32_t)gpp, cg = g32 - pix * (uint32_t)gpp;
+            const uint32_t row = pix / (uint32_t)pad_w, x = pix - row * (uint32_t)pad_w;
+            oi = ((long long)row * (pad_w + 1) + x + 1) * gpp + cg;
+            if (x == 0) reinterpret_cast<uint4*>(out)[oi - gpp] = make_uint4(0, 0, 0, 0);
+            if (gi >= groups - gpp) reinterpret_cast<uint4*>(out)[oi + gpp] = make_uint4(0, 0, 0, 0);
+        }
+        reinterpret_cast<uint4*>(out)[oi] = make_uint4(o[0], o[1], o[2], o[3]);
         if (zero && zero_flag) atomicOr(zero_flag, 1);
     }
 }
@@ -308,19 +344,28 @@ static int pick_bn_conv(int cout) {
     return (per + 15) / 16 * 16;
 }
 
-size_t conv_fp4_workspace_bytes(int batch, int h, int w, int c) { return (size_t)batch * h * w * c / 2 + 256; }
+static bool pairtap_ok(int c, int kw, int stride, int pad, int cout) {
+    (void)cout;
+    return c == 128 && kw == 3 && stride == 1 && pad == 1;
+}
+
+// fm4, with the tap-pair map's one zero pixel per row
+size_t conv_fp4_workspace_bytes(int batch, int h, int w, int c) { return (size_t)batch * h * (w + 1) * c / 2 + 1024; }
 
 // Whether K6 takes a conv: the im2col map's zero fill must be the padding
 // value, channels tile into 128-channel k-blocks, and the filter fits the
 // resident budget.
-bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, int padding, long long rows) {
+bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, int padding, long long rows,
+                      int stride) {
     if (!(padding == 0 || !fm_binary) || c % 128 != 0 || cout % 8 != 0 || rows > 0x7FFFFFFFLL) return false;
     (void)mode;
-    const int kblocks = kh * kw * (c / 128);
+    const bool pt = pairtap_ok(c, kw, stride, padding, cout);
+    const int kblocks = pt ? 2 * kh : kh * kw * (c / 128);
+    const int kbb = pt ? 2 * C6_KB_BYTES : C6_KB_BYTES;
     const int bn = pick_bn_conv(cout);
-    const int breg = ((bn / 2) * 64 + 1023) / 1024 * 1024;
+    const int breg = ((bn / 2) * (pt ? 128 : 64) + 1023) / 1024 * 1024;
     const int g = kblocks % 4 == 0 ? 4 : (kblocks % 3 == 0 ? 3 : (kblocks % 2 == 0 ? 2 : 1));
-    return kblocks * breg <= C6_B_MAX && (C6_RING_BUDGET - kblocks * breg) / (g * C6_KB_BYTES) >= 2;
+    return kblocks * breg <= C6_B_MAX && (C6_RING_BUDGET - kblocks * breg) / (g * kbb) >= 2;
 }
 
 lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
@@ -329,16 +374,21 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
     const int oh = (h + 2 * pad - kh) / stride + 1, ow = (w + 2 * pad - kw) / stride + 1;
     const long long rows = (long long)batch * oh * ow;
     const int k = kh * kw * cch;
-    uint8_t* fm4 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    static const bool no_pt = getenv("LOWBIT_CONV_NO_PAIRTAP") != nullptr;  // tuning experiment knob
+    const bool pt = pairtap_ok(cch, kw, stride, pad, cout) && !no_pt;
+    uint8_t* fm4 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 1023) & ~uintptr_t(1023));
     const long long groups = (long long)batch * h * w * cch / 32;
-    conv_pack_fp4_kernel<<<grid_for(groups, 256), 256, 0, stream>>>(fm, groups, check_zero, fm4, zero_flag);
+    conv_pack_fp4_kernel<<<grid_for(groups, 256), 256, 0, stream>>>(fm, groups, check_zero, fm4, zero_flag,
+                                                                     pt ? w : 0, cch / 32);
     LB_CUDA_TRY(cudaGetLastError());
 
     const WeightsLayout L(b_ternary, cout, k);
+    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
+
     ConvF4Params prm{};
     prm.rows = (int)rows;
     prm.cout = cout;
-    prm.kblocks = kh * kw * (cch / 128);
+    prm.kblocks = pt ? 2 * kh : kh * kw * (cch / 128);
     prm.g = prm.kblocks % 4 == 0 ? 4 : (prm.kblocks % 3 == 0 ? 3 : (prm.kblocks % 2 == 0 ? 2 : 1));
     prm.bn = pick_bn_conv(cout);
     prm.m_tiles = (int)((rows + 2 * C6_BM - 1) / (2 * C6_BM));
@@ -349,28 +399,38 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
     prm.pad = pad;
     prm.kw = kw;
     prm.cblocks = cch / 128;
-    prm.breg = ((prm.bn / 2) * 64 + 1023) / 1024 * 1024;
-    prm.a_st = (C6_RING_BUDGET - prm.kblocks * prm.breg) / (prm.g * C6_KB_BYTES);
+    const int row_bytes = pt ? 128 : 64;  // bytes of one k-block per filter row / output pixel
+    prm.breg = ((prm.bn / 2) * row_bytes + 1023) / 1024 * 1024;
+    prm.a_st = (C6_RING_BUDGET - prm.kblocks * prm.breg) / (prm.g * C6_BM * row_bytes);
     if (prm.a_st > C6_MAX_A_ST) prm.a_st = C6_MAX_A_ST;
     prm.ldc = cout;
     prm.c = out;
     CUtensorMap mb, ma, mc;
-    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
-    if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 64, (uint32_t)(prm.bn / 2),
-                     CU_TENSOR_MAP_SWIZZLE_64B))
-        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
-    if (!make_map_im2col(&ma, fm4, batch, h, w, cch / 2, kh, kw, stride, pad, 64, C6_BM, CU_TENSOR_MAP_SWIZZLE_64B))
-        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeIm2col failed (fp4 feature map)");
+    if (pt) {
+        if (!make_map_filter_pairtap(&mb, wfp4, kh, (uint64_t)L.np, (uint64_t)L.kp4 / 2, (uint32_t)(prm.bn / 2)))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
+        if (!make_map_im2col_pairtap(&ma, fm4, batch, h, w, kh, pad, C6_BM))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeIm2col failed (tap-pair map)");
+    } else {
+        if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 64,
+                         (uint32_t)(prm.bn / 2), CU_TENSOR_MAP_SWIZZLE_64B))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
+        if (!make_map_im2col(&ma, fm4, batch, h, w, cch / 2, kh, kw, stride, pad, 64, C6_BM,
+                             CU_TENSOR_MAP_SWIZZLE_64B))
+            return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeIm2col failed (fp4 feature map)");
+    }
     if (!make_map_2d(&mc, out, (uint64_t)cout, (uint64_t)rows, (uint64_t)cout * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B,
                      CU_TENSOR_MAP_DATA_TYPE_UINT16))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv output");
-    static bool attr = false;
-    if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(conv_fp4_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C6_SMEM));
-        attr = true;
+    static bool attr[2] = {false, false};
+    if (!attr[pt]) {
+        LB_CUDA_TRY(cudaFuncSetAttribute(pt ? conv_fp4_pair_kernel<true> : conv_fp4_pair_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C6_SMEM));
+        attr[pt] = true;
     }
     const int pairs = prm.m_tiles < num_sms() / 2 ? prm.m_tiles : num_sms() / 2;
-    conv_fp4_pair_kernel<<<2 * pairs, C6_THREADS, C6_SMEM, stream>>>(mb, ma, mc, prm);
+    if (pt) conv_fp4_pair_kernel<true><<<2 * pairs, C6_THREADS, C6_SMEM, stream>>>(mb, ma, mc, prm);
+    else conv_fp4_pair_kernel<false><<<2 * pairs, C6_THREADS, C6_SMEM, stream>>>(mb, ma, mc, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

@@ -138,6 +138,23 @@ def test_conv_fp4_binary_and_wide(lb, port):
 
 
 @pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_conv_fp4_tap_pairs(lb, port, mode):
+    """K6's tap-pair form (c = 128, 3x3, stride 1, padding 1): the zero pixel
+    leading each fm4 row, the out-of-bounds zero half of the (dummy, kx = 0)
+    filter pair, narrow and wide rows, several images and n tiles."""
+    da, db = mode_dists(mode)
+    for i, (b, h, w, cout) in enumerate([(1, 1, 1, 8), (2, 3, 2, 16), (3, 5, 7, 40), (1, 9, 33, 300),
+                                         (2, 14, 14, 496), (1, 2, 130, 24)]):
+        fm = port.generate(da, 120 + i, 0, b * h * w, 128).reshape(b, h, w, 128)
+        wt = port.generate(db, 120 + i, 1, 9 * 128, cout)
+        got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), mode == BNN, weights_for(lb, wt, mode), 3, 3, 1,
+                               1).cpu().numpy()
+        for img in range(b):
+            want = port.direct_conv(fm[img], mode == BNN, wt, 3, 3, 1, 1)
+            assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, cout)
+
+
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
 def test_gemm_from_int8(lb, port, mode):
     da, db = mode_dists(mode)
     for i, (m, n, k) in enumerate([(1, 1, 16), (17, 9, 512), (300, 520, 1008), (360, 96, 256), (129, 257, 4096),
