@@ -249,6 +249,8 @@ lowbit_status lowbit_generate(int dist, unsigned long long seed, int matrix_id, 
 int lowbit_debug_pair_stats(unsigned long long* out16);
 /* Same for the fp4 pair kernel (LOWBIT_DEBUG_FP4=8). */
 int lowbit_debug_fp4_stats(unsigned long long* out16);
+/* Tuning aid: per-tile event clocks of K6's first leader CTA (LOWBIT_CONV_DEBUG & 32); 0 on success. */
+int lowbit_debug_conv_trace(unsigned long long* out1024);
 
 #ifdef __cplusplus
 }

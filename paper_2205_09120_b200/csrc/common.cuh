@@ -60,6 +60,23 @@ LB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Non-blocking phase test (mbarrier.test_wait): for a barrier that is usually
+// complete already, polling it avoids try_wait's fixed cost.
+LB_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+LB_DEV void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
+    while (!mbar_test_wait(bar, parity)) {
+    }
+}
 LB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
@@ -264,14 +281,6 @@ LB_DEV void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, uint32_t m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_leader_form), "r"(x), "r"(y), "h"(cta_mask)
         : "memory");
 }
-// 3-D tiled TMA load whose completion bytes land on the LEADER CTA's mbarrier (pair mode).
-LB_DEV void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int x, int y, int z) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-        "%5}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y), "r"(z)
-        : "memory");
-}
 // im2col-mode TMA (pair form): 4-D NHWC map {c, w, h, n} + filter-tap offsets.
 LB_DEV void tma_load_im2col_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c, int w, int h,
                                     int n, uint16_t off_w, uint16_t off_h) {
@@ -339,6 +348,12 @@ LB_DEV void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
                  "r"(src), "r"(x), "r"(y)
+                 : "memory");
+}
+LB_DEV void tma_store_4d(const CUtensorMap* map, uint32_t src, int x, int y, int z, int w) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(x), "r"(y), "r"(z), "r"(w)
                  : "memory");
 }
 LB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }

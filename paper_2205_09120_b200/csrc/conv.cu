@@ -88,7 +88,7 @@ __global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict
 }  // namespace lb
 
 namespace lb {
-size_t conv_fp4_workspace_bytes(int batch, int h, int w, int c);
+size_t conv_fp4_workspace_bytes(int batch, int h, int w, int c, int pad);
 bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, int padding, long long rows,
                       int stride);
 lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
@@ -152,7 +152,7 @@ extern "C" size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int 
                                                 int padding) {
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
     const size_t planes = (size_t)rows * lowbit_plane_pitch(kh * kw * c) * (mode == LOWBIT_BNN ? 1 : 2) + 256;
-    const size_t fm4 = lb::conv_fp4_workspace_bytes(batch, h, w, c);  // K6's packed fp4 feature map
+    const size_t fm4 = lb::conv_fp4_workspace_bytes(batch, h, w, c, padding);  // K6's packed fp4 feature map
     return planes > fm4 ? planes : fm4;
 }
 

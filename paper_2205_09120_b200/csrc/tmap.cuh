@@ -34,6 +34,25 @@ inline bool make_map_2d(CUtensorMap* map, const void* base, uint64_t dim0, uint6
     return r == CUDA_SUCCESS;
 }
 
+// The conv output [batch, oh, ow, cout] int16 as a 4-D map for boxes of
+// {16 channels, 32 pixels of one output row}: boxes may start left of x = 0
+// or run past ow / oh — the clipped elements are not written — which lets a
+// run of consecutive padded positions be stored row by row.
+// box_cols 16 (32-byte swizzle) or 64 (128-byte swizzle).
+inline bool make_map_conv_out(CUtensorMap* map, void* base, int batch, int oh, int ow, int cout, uint32_t box_cols) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)cout, (cuuint64_t)ow, (cuuint64_t)oh, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)cout * 2, (cuuint64_t)ow * cout * 2, (cuuint64_t)oh * ow * cout * 2};
+    cuuint32_t box[4] = {box_cols, 32, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // 4-D NHWC int8 im2col map for implicit-GeMM convolution (fprop): lower
 // corner -pad, upper corner pad - (k-1), traversal stride = conv stride
 // (the CUTLASS convention, cutlass/conv/collective/detail.hpp).  Each load
@@ -57,54 +76,6 @@ inline bool make_map_im2col(CUtensorMap* map, const void* base, int n, int h, in
     cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, lower, upper,
                     channels, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// "Tap-pair" im2col map over a packed fp4 NHWC map whose rows lead with one
-// zero pixel (row pitch (w+1) pixels of 64 bytes, one more zero pixel at the end): each virtual pixel
-// is 128 bytes = two horizontally adjacent pixels (stride 64 bytes), so one
-// load brings two taps of a 3-wide filter for 128 output pixels.  Stride 1,
-// padding 1 (the left edge's zero fill must cover exactly the padding).
-inline bool make_map_im2col_pairtap(CUtensorMap* map, const void* base, int n, int h, int w, int kh, int pad,
-                                    uint32_t pixels) {
-    static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
-    }
-    if (!fn) return false;
-    cuuint64_t dims[4] = {128, (cuuint64_t)w + 1, (cuuint64_t)h, (cuuint64_t)n};
-    cuuint64_t strides[3] = {64, (cuuint64_t)(w + 1) * 64, (cuuint64_t)h * (w + 1) * 64};
-    // map x' = x + 1 (the zero pixel leads each row): from the window's first
-    // tap x, offset 0 covers (x-1, x) for the (zero dummy, kx = 0) pair and
-    // offset 2 covers (x+1, x+2) for (kx = 1, kx = 2)
-    int lower[2] = {-pad, -pad};
-    int upper[2] = {pad - 3, pad - (kh - 1)};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, lower, upper, 128,
-                    pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// 3-D view of the prepared fp4 filter rows for the tap pairs: {192 bytes = the
-// three taps (128 channels each) of one filter row, ky (kh), output channel}.
-// A 128-byte box at x = -64 reads (zero, tap (ky,0)) — the out-of-bounds half
-// is zero-filled — and at x = 64 reads (tap (ky,1), tap (ky,2)).
-inline bool make_map_filter_pairtap(CUtensorMap* map, const void* base, int kh, uint64_t rows, uint64_t row_bytes,
-                                    uint32_t box_rows) {
-    auto fn = get_encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[3] = {192, (cuuint64_t)kh, rows};
-    cuuint64_t strides[2] = {192, row_bytes};
-    cuuint32_t box[3] = {128, 1, box_rows};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }

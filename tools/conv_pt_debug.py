@@ -9,7 +9,7 @@ import paper_2205_09120_b200 as lb
 from oracle.oracle import Port
 
 p = Port()
-b, h, w, c, cout = int(sys.argv[1]) if len(sys.argv) > 1 else 1, 6, 7, 128, 8
+b, h, w, c, cout = int(sys.argv[1]) if len(sys.argv) > 1 else 2, 6, 7, 128, 8
 fm = p.generate(0, 5, 0, b * h * w, c).reshape(b, h, w, c)
 wt = p.generate(0, 5, 1, 9 * c, cout)
 bp = lb.encode_ternary(torch.from_numpy(wt).cuda())
