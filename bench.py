@@ -13,7 +13,7 @@ data path (north_star: NCCL only gathers outputs where a test requires it).
 
 One step = one gemm_lowbit over this rank's rows with the encoded A planes
 resident in HBM (the reference timing policy: encode and pack_b excluded,
-bench.cpp:49,58).  L2 is flushed (256 MiB write) between steps, outside the
+bench.cpp:49,58).  L2 is flushed (256 MiB write + read) between steps, outside the
 CUDA events that time each step's kernel.  value = 2*M*N*K / max-over-ranks of
 the per-step device time, in TOPS.
 
@@ -300,7 +300,7 @@ def main():
         lb.gemm_lowbit(mode, ap_, w, (m, N, K), kernel=kernel, out=c)
 
     for _ in range(args.warmup):
-        flush.zero_()
+        flush_l2(flush)
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -309,7 +309,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            flush.zero_()
+            flush_l2(flush)
             ev[i][0].record()
             step()
             ev[i][1].record()
@@ -448,7 +448,7 @@ def main():
             "data": "synthetic (counter-based splitmix64 generator, BASELINE.json distributions)",
             "config": {"workload": f"{args.config}: {MODE_NAME[mode]} GeMM M={M} N={N} K={K} int16 C, "
                                    f"A rows sharded over {world} GPU(s), B replicated",
-                       "global_rows": M, "rows_per_rank": M // world, "l2": "flushed (256 MiB write) between steps",
+                       "global_rows": M, "rows_per_rank": M // world, "l2": "flushed between steps (256 MiB write + read back, clean lines)",
                        "kernel": {1: "bitserial", 2: "tensor (fp4 K5)" if fp4 else "tensor (int8 K3)",
                                   4: "tensor (int8 K3)"}.get(chosen, str(chosen)),
                        "a_layout": {2: "nibbles (B200 nibble-interleaved bit planes from K1)",
@@ -463,13 +463,23 @@ def main():
         dist.destroy_process_group()
 
 
+def flush_l2(flush):
+    """Evict L2 between timed steps: write a 256 MiB buffer (2x the 126 MB L2),
+    then read it back so the lines left in L2 are clean — otherwise the next
+    timed kernel pays for writing the flush buffer's dirty lines to HBM
+    (~126 MB, ~19 us: half of a c4 conv)."""
+    import torch
+    flush.zero_()
+    flush.view(torch.int64).sum()
+
+
 def time_device(torch, fn, flush, reps=10):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush_l2(flush)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
@@ -510,7 +520,7 @@ def graph_time_flushed(torch, fn, flush, reps=10):
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush_l2(flush)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         g.replay()

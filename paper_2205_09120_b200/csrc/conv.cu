@@ -94,6 +94,11 @@ bool conv_fp4_applies(int mode, int fm_binary, int c, int cout, int kh, int kw, 
 lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
                               int pad, int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
                               void* workspace, int* zero_flag, cudaStream_t stream);
+bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int kw, int stride, int pad,
+                       long long batch);
+lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int pad,
+                               int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
+                               int* zero_flag, cudaStream_t stream);
 lowbit_status launch_conv_pair_im2col(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
                                       int pad, const void* weights, int b_ternary, int cout, int16_t* out,
                                       cudaStream_t stream);
@@ -170,6 +175,14 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
     // k-blocks.  BNN keeps the bit path: its padding is +-1 and a 0 activation
     // must raise ZeroInBinaryInput (conv.cpp:13, core.cpp:23).
     const bool pad_is_zero = padding == 0 || !fm_binary;
+    // K7, fused halo convolution on the fp4 tensor cores (stride 1, no workspace)
+    static const bool no_halo = getenv("LOWBIT_CONV_NO_HALO") != nullptr;  // tuning experiment knob
+    if ((kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) && !no_halo &&
+        lb::conv_halo_applies(fm_binary, h, w, c, cout, kh, kw, stride, padding, batch) &&
+        (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
+        (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+        return lb::launch_conv_halo(fm, batch, h, w, c, kh, kw, padding, mode == LOWBIT_BNN && fm_binary, weights,
+                                    b_ternary, cout, out, zero_flag, (cudaStream_t)stream);
     // K6, fp4 implicit GeMM over a packed fp4 copy of the feature map (workspace)
     if ((kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) && workspace &&
         lb::conv_fp4_applies(mode, fm_binary, c, cout, kh, kw, padding, rows, stride) &&

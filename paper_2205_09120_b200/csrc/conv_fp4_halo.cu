@@ -1,0 +1,567 @@
+// conv_fp4_halo.cu — K7: fused halo convolution on the fp4 tensor cores
+// (stride 1, the int8 feature map read once, no packed copy, no im2col).
+//
+// conv2d_lowbit (conv.cpp:33-59) is im2col -> encode -> pack_b -> gemm_lowbit
+// with GeMM depth index k = (ky*kw + kx)*C + c (conv.cpp:18-27).  Here one
+// kernel does all of it:
+//
+//   * Output positions are laid out on a padded grid of pitch P = 32, 64 or
+//     128 >= W + 2*pad: a CTA tile is R = 128/P whole output rows of one
+//     image (position i = ry*P + ox).  Its input "halo" is the R + kh - 1
+//     padded input rows starting at y0 - pad, P pixels each starting at
+//     x = -pad: ONE 4-D TMA box of the int8 NHWC map per 128-channel block,
+//     whose out-of-image elements read as zero — the padding.
+//   * Converter warps turn the int8 halo into packed e2m1 (+1 -> 0x2,
+//     -1 -> 0xA, 0 -> 0x0, two channels per byte) in a 64-byte-swizzled
+//     shared-memory tile: halo position j is UMMA row j.
+//   * Filter tap (ky, kx) of output position i reads halo position
+//     i + ky*P + kx, so the A operand of that tap is the halo tile's UMMA
+//     descriptor advanced by ky*P + kx rows (the swizzle is a function of
+//     the absolute address; tools/micro/halo_check.cu) — no im2col exists
+//     anywhere.  Positions with ox >= OW (or rows past OH) are computed and
+//     dropped; their taps may read a few rows past the halo (garbage-in,
+//     never stored).
+//   * The filter (prepared weights, fp4 section, K-major) stays resident in
+//     shared memory; tcgen05.mma.cta_group::2.kind::mxf4.block_scale with
+//     unit scales and f32 accumulators (exact: |partial sums| <= k <= 32767).
+//   * The epilogue converts each accumulator lane (one output pixel) to
+//     int16 and stores it straight to global memory (no staging: shared
+//     memory bandwidth is the scarce resource here — the N = cout = 128
+//     MMAs read 6 KB of operands per CTA per 64 cycles, ~75% of it).
+//   * Encoding: +-1 activations become +-0.5 (e2m1 0x1 / 0x9 = the int8 byte
+//     AND 0x09), the filter stays +-1.0, and the epilogue doubles the exact
+//     half-integer sums.
+//
+// Warp roles per CTA (608 threads): 0-7 epilogue (warps 0-3 drain even
+// tiles, 4-7 odd ones, one warp per TMEM lane quarter), 8-15 converters, 16
+// TMA producer (raw halo + filter), 17-18 UMMA issuers on alternate tiles
+// (leader CTA; warp 17 also owns TMEM).
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "encode.cuh"
+#include "layout.cuh"
+#include "tmap.cuh"
+
+namespace lb {
+
+constexpr int H7_BM = 128;        // output positions per CTA tile (256 per pair)
+constexpr int H7_NCONV = 8;       // converter warps
+constexpr int H7_W_CONV = 8, H7_W_PROD = H7_W_CONV + H7_NCONV, H7_W_MMA = H7_W_PROD + 1;
+constexpr int H7_THREADS = 32 * (H7_W_MMA + 2);
+constexpr int H7_MAX_BN = 240;    // cout per tile: accumulators + scales <= 512 TMEM columns
+constexpr uint32_t H7_SF_COL = 480;
+constexpr int H7_SMEM = 227 * 1024;
+constexpr int H7_BAR_BYTES = 1024;  // barriers + the k-block offset table
+constexpr int H7_MAX_KB = 96;       // k-blocks (taps x channel blocks) the offset table holds
+constexpr int H7_MAX_ST = 4;        // raw / fp4 ring depth cap
+constexpr int H7_RAW_MAX = 64 * 1024;
+
+struct HaloParams {
+    int batch, h, w, oh, ow, pad, kw, cblocks;
+    int P, log2p, R, rows_h;   // position pitch (32, 64 or 128), output rows per CTA tile, halo rows
+    int tpi, ctiles, ptiles;   // CTA tiles per image, CTA tiles, pair tiles
+    int cout, bn, n_tiles, kblocks;
+    int breg;                  // bytes of one resident filter k-block (1 KB aligned)
+    int raw_cb;                // bytes of one channel block of a raw stage
+    int f4_cb;                 // bytes of one channel block of an fp4 halo (1 KB aligned)
+    int raw_st, f4_st;         // ring depths
+    int nacc, acc_cols;        // TMEM accumulators and their column stride
+    int k33;                   // 3x3 filter over one channel block: the unrolled issue loop
+    int check_zero;            // binary map: a 0 activation sets *zero_flag (core.cpp:23)
+    int dbg;                   // timing experiments (LOWBIT_HALO_DEBUG): 1 no stores, 2 no MMAs, 4 no conversion,
+                               // 64 epilogue ignores tmem_full, 128 epilogue drains nothing, 32 trace,
+                               // 2048 no tiles (setup + teardown only)
+    int16_t* out;
+    int* zero_flag;
+};
+
+// dbg & 32: per-tile event times (clock64) of pair 0's leader CTA, read by lowbit_debug_halo_trace
+__device__ unsigned long long g_halo_trace[16 * 64];
+#define H7_TRACE(ev, i) \
+    if ((prm.dbg & 32) && pair == 0 && leader && (i) < 64) g_halo_trace[(ev) * 64 + (i)] = clock64()
+
+LB_DEV uint64_t h7_desc_sw64(uint32_t smem_addr) {  // K-major, 64-byte rows, 8-row atoms every 512 B
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;
+    d |= (uint64_t)(512u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)4u << 61;  // SWIZZLE_64B
+    return d;
+}
+
+// 16 int8 {-1, 0, +1} -> 16 packed e2m1 (8 bytes; channel 2i in the low
+// nibble of byte i) encoding +-1 as +-0.5 (0x1 / 0x9): the code is the int8
+// byte ANDed with 0x09 (0x01 -> 0x1, 0xFF -> 0x9, 0x00 -> 0x0), so the whole
+// conversion is AND, SHF + OR per word and one PRMT per word pair.  The
+// filter stays +-1.0, every product is +-0.5, and the f32 sums are
+// half-integers of magnitude <= 16383.5 (exact); the epilogue doubles them.
+LB_DEV uint32_t h7_pack8(uint32_t x0, uint32_t x1) {
+    const uint32_t c0 = x0 & 0x09090909u, c1 = x1 & 0x09090909u;
+    const uint32_t t0 = c0 | (c0 >> 4), t1 = c1 | (c1 >> 4);  // byte 0 = ch0 | ch1 << 4, byte 2 = ch2 | ch3 << 4
+    return __byte_perm(t0, t1, 0x6420);
+}
+// all 16 bytes nonzero (a binary map holds no 0, core.cpp:23)
+LB_DEV bool h7_all_nonzero(uint4 v) {
+    return (nonzero_msb(v.x) & nonzero_msb(v.y) & nonzero_msb(v.z) & nonzero_msb(v.w)) == 0x80808080u;
+}
+
+// waits of the non-issuing roles: suspend-hinted try_wait (dbg & 1024: plain try_wait)
+LB_DEV void h7_wait(int dbg, uint64_t* bar, uint32_t parity) {
+    if (dbg & 1024) mbar_wait(bar, parity);
+    else mbar_wait_sleep(bar, parity);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
+    conv_fp4_halo_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_raw,
+                         const HaloParams prm) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int CB = prm.cblocks;
+    const int raw_stage = CB * prm.raw_cb, f4_stage = CB * prm.f4_cb;
+    uint8_t* sB = smem;                                      // resident filter: kblocks x breg
+    uint8_t* sRaw = sB + prm.kblocks * prm.breg;             // raw int8 halo ring
+    uint8_t* sF4 = sRaw + prm.raw_st * raw_stage;            // fp4 halo ring (the UMMA A operand)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sF4 + prm.f4_st * f4_stage);
+    uint64_t* raw_full = bars;            // local: TMA landed the raw halo
+    uint64_t* raw_empty = bars + 4;       // local: the converter warps are done with it
+    uint64_t* a_full = bars + 8;          // leader: fp4 halos of both CTAs written (all converter warps)
+    uint64_t* a_empty = bars + 12;        // local: the pair's MMAs are done with the fp4 halo
+    uint64_t* b_full = bars + 16;         // leader: the filter of this n tile landed (both CTAs)
+    uint64_t* b_empty = bars + 17;        // local: both issuers' MMAs done with the filter
+    uint64_t* tmem_full = bars + 18;      // local (3): accumulator complete
+    uint64_t* tmem_empty = bars + 21;     // leader (3): the tile's 8 epilogue warps (4 per CTA) drained it
+    uint64_t* sf_ready = bars + 24;       // leader: unit scales written (16 warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+    uint32_t* kb_aoff = reinterpret_cast<uint32_t*>(bars + 32);  // k-block -> A row offset (16-byte units)
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int bn = prm.bn, bnh = bn >> 1;
+    const int my_tiles = (prm.ptiles > pair && !(prm.dbg & 2048)) ? (prm.ptiles - pair + npairs - 1) / npairs : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < H7_MAX_ST; ++s) {
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&raw_empty[s], H7_NCONV);
+            mbar_init(&a_full[s], 2 * H7_NCONV);
+            mbar_init(&a_empty[s], 1);
+        }
+        mbar_init(b_full, 1);
+        mbar_init(b_empty, 2);
+        for (int a = 0; a < 3; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 8);
+        }
+        mbar_init(sf_ready, 16);
+        fence_barrier_init();
+    }
+    if (warp == H7_W_PROD && lane == 0) {
+        tma_prefetch_desc(&tmap_raw);
+        tma_prefetch_desc(&tmap_b);
+    }
+    if (warp == H7_W_MMA) {
+        tmem_alloc_pair<512>(tmem_slot);
+        for (int kb = lane; kb < prm.kblocks; kb += 32) {  // tap (ky,kx), channel block cb
+            const int tap = kb / CB, cb = kb - tap * CB;
+            const int ky = tap / prm.kw, kx = tap - ky * prm.kw;
+            kb_aoff[kb] = ((uint32_t)(cb * prm.f4_cb) + (uint32_t)(ky * prm.P + kx) * 64u) >> 4;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == H7_W_PROD) {
+        // ===================== TMA producer (both CTAs): filter + raw halos =====================
+        if (lane == 0 && my_tiles > 0) {
+            const uint32_t b_full0 = mapa_shared(smem_u32(b_full), 0);
+            uint32_t t = 0;
+            for (int nt = 0; nt < prm.n_tiles; ++nt) {
+                h7_wait(prm.dbg, b_empty, (nt & 1) ^ 1);
+                if (leader) mbar_arrive_expect_tx(b_full, (uint32_t)prm.kblocks * bn * 64);
+                const int brow = nt * bn + (int)rank * bnh;
+                for (int kb = 0; kb < prm.kblocks; ++kb)
+                    tma_load_2d_pair(smem_u32(sB + kb * prm.breg), &tmap_b, b_full0, kb * 64, brow);
+                for (int i = 0; i < my_tiles; ++i, ++t) {
+                    const uint32_t s = t % prm.raw_st;
+                    h7_wait(prm.dbg, &raw_empty[s], ((t / prm.raw_st) & 1) ^ 1);
+                    if (nt == 0) H7_TRACE(0, i);
+                    mbar_arrive_expect_tx(&raw_full[s], (uint32_t)raw_stage);
+                    const int ct = (pair + i * npairs) * 2 + (int)rank;  // this CTA's tile
+                    int img = ct / prm.tpi;
+                    int y0 = (ct - img * prm.tpi) * prm.R;
+                    if (ct >= prm.ctiles) img = prm.batch - 1, y0 = 0;  // odd tail: any real box, never stored
+                    for (int cb = 0; cb < CB; ++cb)
+                        tma_load_4d(smem_u32(sRaw + s * raw_stage + cb * prm.raw_cb), &tmap_raw,
+                                    smem_u32(&raw_full[s]), cb * 128, -prm.pad, y0 - prm.pad, img);
+                }
+            }
+        }
+    } else if (warp >= H7_W_CONV && warp < H7_W_PROD) {
+        // ===================== converters (both CTAs): raw int8 halo -> fp4 halo =====================
+        const int cw = warp - H7_W_CONV;
+        const uint32_t a_full0 = mapa_shared(smem_u32(&a_full[0]), 0);
+        // loop constants in registers (kernel parameters would be re-read after
+        // every shared-memory store: the stores' asm clobbers memory)
+        const int P = prm.P, lp = prm.log2p, rows_h = prm.rows_h, raw_st = prm.raw_st, f4_st = prm.f4_st;
+        const int raw_cb = prm.raw_cb, f4_cb = prm.f4_cb, tpi = prm.tpi, R = prm.R, ctiles = prm.ctiles;
+        const bool convert = !(prm.dbg & 4);
+        const int dbg = prm.dbg;
+        const int npos = rows_h * P;             // a multiple of 32
+        constexpr int STEP = 4 * H7_NCONV;     // positions per iteration of all converter warps
+        const int nfull = npos / (8 * STEP), nrem = (npos % (8 * STEP)) / STEP;  // batches of 8 iterations, leftover
+        const int chunk = lane & 7;              // 16 channels of one position
+        const int j0 = cw * 4 + (lane >> 3);     // this lane's first position; then every STEP-th
+        auto raw_off = [](int j) -> uint32_t { return (uint32_t)j << 7; };  // raw layout: [position] x 128 B
+        // SW64: 16-byte unit u of row j at j*64 + ((u ^ ((j >> 1) & 3)) << 4); (j >> 1) & 3 is the
+        // same for all of this lane's positions (they step by a multiple of 8)
+        const uint32_t swz = ((((uint32_t)chunk >> 1) ^ (((uint32_t)j0 >> 1) & 3u)) << 4) + (chunk & 1) * 8;
+        bool zero = false;
+        uint32_t t = 0;
+        for (int nt = 0; nt < prm.n_tiles; ++nt)
+            for (int i = 0; i < my_tiles; ++i, ++t) {
+                const uint32_t rs = t % raw_st, fs = t % f4_st;
+                h7_wait(dbg, &raw_full[rs], (t / raw_st) & 1);
+                if (cw == 0 && lane == 0) H7_TRACE(1, t);
+                h7_wait(dbg, &a_empty[fs], ((t / f4_st) & 1) ^ 1);
+                if (cw == 0 && lane == 0) H7_TRACE(2, t);
+                if (convert)
+                    for (int cb = 0; cb < CB; ++cb) {
+                        const uint32_t src = smem_u32(sRaw + rs * raw_stage + cb * raw_cb) + chunk * 16;
+                        const uint32_t dst = smem_u32(sF4 + fs * f4_stage + cb * f4_cb) + swz;
+                        for (int b = 0; b < nfull; ++b) {  // eight loads in flight, then eight stores
+                            const int jb = j0 + b * 8 * STEP;
+                            uint4 v[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) v[q] = lds_v4(src + raw_off(jb + STEP * q));
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                sts_v2(dst + (uint32_t)(jb + STEP * q) * 64u, h7_pack8(v[q].x, v[q].y),
+                                       h7_pack8(v[q].z, v[q].w));
+                        }
+                        for (int q = 0; q < nrem; ++q) {
+                            const int j = j0 + nfull * 8 * STEP + STEP * q;
+                            const uint4 v = lds_v4(src + raw_off(j));
+                            sts_v2(dst + (uint32_t)j * 64u, h7_pack8(v.x, v.y), h7_pack8(v.z, v.w));
+                        }
+                    }
+                if (prm.check_zero && nt == 0) {  // binary map: any 0 in a real pixel (not padding)?
+                    const int ct = (pair + i * npairs) * 2 + (int)rank;
+                    const int img = ct / tpi;
+                    const int y0 = (ct - img * tpi) * R;
+                    if (ct < ctiles)
+                        for (int cb = 0; cb < CB; ++cb) {
+                            const uint32_t src = smem_u32(sRaw + rs * raw_stage + cb * raw_cb) + chunk * 16;
+                            for (int j = j0; j < npos; j += STEP) {
+                                const int y = y0 - prm.pad + (j >> lp), x = (j & (P - 1)) - prm.pad;
+                                if (y >= 0 && y < prm.h && x >= 0 && x < prm.w && !h7_all_nonzero(lds_v4(src + raw_off(j))))
+                                    zero = true;
+                            }
+                        }
+                }
+                if (cw == 0 && lane == 0) H7_TRACE(15, t);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (cw == 0 && lane == 0) H7_TRACE(3, t);
+                if (lane == 0) {
+                    mbar_arrive(&raw_empty[rs]);
+                    mbar_arrive_cluster(a_full0 + fs * 8);
+                }
+            }
+        if (zero && prm.zero_flag) atomicOr(prm.zero_flag, 1);
+    } else if (warp >= H7_W_MMA) {
+        // ===================== UMMA issuers (leader CTA): alternate tiles =====================
+        // A waiting issuer thread stalls for ~300 cycles per mbarrier wait while
+        // only a few 64-cycle (N = 128) MMAs are queued; two issuers keep the
+        // tensor pipe fed across each other's waits.
+        const int which = warp - H7_W_MMA;
+        if (leader && my_tiles > 0) {
+            const uint32_t idesc = idesc_mxf4(2 * H7_BM, (uint32_t)bn);
+            const uint32_t sf = tmem_base + H7_SF_COL;
+            const int nkb = prm.kblocks;
+            const uint32_t breg16 = (uint32_t)prm.breg >> 4;
+            const uint64_t bd0 = h7_desc_sw64(smem_u32(sB));
+            const uint32_t p4 = (uint32_t)prm.P * 4;  // one halo row of positions in 16-byte units
+            const bool skip_mma = (prm.dbg & 2) != 0;
+            const bool kx_off = !(prm.dbg & 8);  // timing experiment: 8-row-aligned A for every tap (wrong results)
+            mbar_wait(sf_ready, 0);
+            tc_fence_after();
+            uint32_t t = 0;
+            int acc = 0;
+            for (int nt = 0; nt < prm.n_tiles; ++nt) {
+                mbar_wait(b_full, nt & 1);
+                tc_fence_after();
+                for (int i = 0; i < my_tiles; ++i, ++t) {
+                    const int u = (int)t;
+                    const int a = acc;
+                    if (++acc == prm.nacc) acc = 0;
+                    if ((u & 1) != which) continue;  // the other issuer's tile
+                    mbar_wait_poll(&tmem_empty[a], ((uint32_t)(u / prm.nacc) & 1) ^ 1);
+                    if (lane == 0) H7_TRACE(4, t);
+                    const uint32_t fs = t % prm.f4_st;
+                    mbar_wait_poll(&a_full[fs], (t / prm.f4_st) & 1);
+                    tc_fence_after();
+                    if (lane == 0) H7_TRACE(5, t);
+                    if (lane == 0) {
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(a * prm.acc_cols);
+                        const uint64_t ad0 = h7_desc_sw64(smem_u32(sF4 + fs * f4_stage));
+                        if (prm.k33) {
+#pragma unroll
+                            for (int kb = 0; kb < 9; ++kb) {
+                                const uint64_t ad = ad0 + (uint32_t)((kb / 3) * p4 + (kx_off ? (kb % 3) * 4 : 0));
+                                const uint64_t bd = bd0 + (uint32_t)(kb * breg16);
+                                if (!skip_mma || kb == 0) {
+                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
+                                    umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
+                                }
+                            }
+                        } else {
+                            for (int kb = 0; kb < nkb; ++kb) {
+                                const uint64_t ad = ad0 + kb_aoff[kb];
+                                const uint64_t bd = bd0 + (uint64_t)kb * breg16;
+                                if (!skip_mma || kb == 0) {
+                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
+                                    umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
+                                }
+                            }
+                        }
+                        umma_commit_pair(&a_empty[fs], 0x3);
+                        umma_commit_pair(&tmem_full[a], 0x3);
+                        H7_TRACE(6, t);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) umma_commit_pair(b_empty, 0x3);
+                __syncwarp();
+            }
+        }
+    } else {
+        // ===================== epilogue (both CTAs): warps 0-7 =====================
+        const int wq = warp & 3;     // TMEM lane quarter = 32 output positions
+        const int half = warp >> 2;  // which warp group: even or odd tiles
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        tmem_st_32x32b_x8_fill(tmem_base + lane_base + H7_SF_COL, 0x7F7F7F7Fu);  // unit UE8M0 scales
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(sf_ready), 0));
+        const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
+        const int nch = bn / 16;
+        // The warp's 32 positions are 32 consecutive pixels of one output row
+        // (P is a multiple of 32); lane l holds pixel l's columns and stores
+        // them as 32-byte vectors (one full sector per lane).  Staging through
+        // shared memory for coalesced 128-byte rows (or an 8 x 8 shuffle
+        // transpose, which runs on the same crossbar) measured slower: shared
+        // memory bandwidth is the kernel's binding resource.
+        const int ry = (wq * 32) / prm.P, ox0 = (wq * 32) % prm.P;
+        const bool v8ok = (prm.cout & 15) == 0;  // 32-byte aligned pixel rows
+        int u = 0;
+        for (int nt = 0; nt < prm.n_tiles; ++nt)
+            for (int i = 0; i < my_tiles; ++i, ++u) {
+                if ((u & 1) != half) continue;  // the two warp groups drain alternate tiles
+                const int acc = u % prm.nacc;
+                const uint32_t acc_phase = (uint32_t)(u / prm.nacc) & 1;
+                const int ct = (pair + i * npairs) * 2 + (int)rank;
+                const int img = ct / prm.tpi;
+                const int oy = (ct - img * prm.tpi) * prm.R + ry;
+                const bool row_ok = ct < prm.ctiles && oy < prm.oh && !(prm.dbg & 1);
+                const bool col_ok0 = row_ok && ox0 + lane < prm.ow;  // this lane's pixel exists
+                int16_t* orow = prm.out + (((long long)img * prm.oh + oy) * prm.ow + ox0) * prm.cout + nt * bn;
+                const int cmax = prm.cout - nt * bn;  // valid columns of this n tile
+                if (!(prm.dbg & 64)) h7_wait(prm.dbg, &tmem_full[acc], acc_phase);
+                tc_fence_after();
+                if (wq == 0 && lane == 0) H7_TRACE(7, u);
+                if (prm.dbg & 128) {  // timing experiment: drain nothing
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
+                    continue;
+                }
+                const uint32_t tacc = tmem_base + lane_base + (uint32_t)(acc * prm.acc_cols);
+                for (int g = 0; g < nch; g += 4) {
+                    const int nc = nch - g < 4 ? nch - g : 4;
+                    // unit q (16 bytes) = columns 16g + 8q .. +7 of this lane's pixel; the f32
+                    // sums are half-integers: 2x + 1.5*2^23 is exact and its low 16 bits are
+                    // the int16 result (see gemm_fp4_pair.cu)
+#pragma unroll
+                    for (int hc = 0; hc < 2; ++hc) {
+                        uint32_t v[2][16];
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+                            if (2 * hc + c < nc) tmem_ld_32x32b_x16(tacc + (g + 2 * hc + c) * 16, v[c]);
+                        tmem_ld_wait();
+                        if (wq == 0 && lane == 0 && g == 0) H7_TRACE(10 + 2 * hc, u);
+                        if (hc == 1 && g + 4 >= nch) {  // the tile's last TMEM read: hand the accumulator back
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
+                            if (wq == 0 && lane == 0) H7_TRACE(8, u);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            if (2 * hc + c >= nc) break;
+                            uint32_t w8[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                w8[q] = __byte_perm(
+                                    __float_as_uint(fmaf(__uint_as_float(v[c][2 * q]), 2.0f, 12582912.0f)),
+                                    __float_as_uint(fmaf(__uint_as_float(v[c][2 * q + 1]), 2.0f, 12582912.0f)),
+                                    0x5410);
+                            // direct 32-byte stores (one full sector per lane): no shared-memory
+                            // traffic, which the MMA operand reads need (smem-bandwidth bound)
+                            const int col = (g + 2 * hc + c) * 16;
+                            if (col_ok0 && col < cmax) {
+                                int16_t* dst = orow + (long long)lane * prm.cout + col;
+                                if (v8ok && col + 16 <= cmax) {
+                                    stg_v8(dst, w8);
+                                } else {
+                                    stg_v4(dst, w8[0], w8[1], w8[2], w8[3]);
+                                    if (col + 8 < cmax) stg_v4(dst + 8, w8[4], w8[5], w8[6], w8[7]);
+                                }
+                            }
+                        }
+                        if (wq == 0 && lane == 0 && g == 0) H7_TRACE(11 + 2 * hc, u);
+                    }
+                    if (wq == 0 && lane == 0 && g == 0) H7_TRACE(14, u);
+                }
+                if (wq == 0 && lane == 0) H7_TRACE(9, u);
+            }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == H7_W_MMA) {
+        tc_fence_after();
+        tmem_dealloc_pair<512>(tmem_base);
+    }
+}
+
+static int h7_pick_bn(int cout) {
+    const int tiles = (cout + H7_MAX_BN - 1) / H7_MAX_BN;
+    const int per = (cout + tiles - 1) / tiles;
+    return (per + 15) / 16 * 16;
+}
+
+namespace {
+struct HaloGeom {
+    int P, R, rows_h, bn, breg, raw_cb, f4_cb, raw_st, f4_st, kblocks;
+    bool ok;
+};
+HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, int pad) {
+    HaloGeom g{};
+    g.ok = false;
+    const int wp = w + 2 * pad;
+    if (stride != 1 || c % 128 != 0 || cout % 8 != 0 || kw > 9 || wp > 128 || h + 2 * pad < kh || wp < kw)
+        return g;
+    g.P = wp <= 32 ? 32 : (wp <= 64 ? 64 : 128);
+    g.R = H7_BM / g.P;
+    g.rows_h = g.R + kh - 1;
+    if (g.rows_h > 256) return g;
+    const int cb = c / 128;
+    g.kblocks = kh * kw * cb;
+    g.bn = h7_pick_bn(cout);
+    g.breg = ((g.bn / 2) * 64 + 1023) / 1024 * 1024;
+    g.raw_cb = g.rows_h * g.P * 128;
+    g.f4_cb = ((g.rows_h * g.P + 8) * 64 + 1023) / 1024 * 1024;  // + the taps' over-read past the halo
+    if (g.kblocks > H7_MAX_KB || cb * g.raw_cb > H7_RAW_MAX) return g;
+    const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - g.kblocks * g.breg;
+    // ring depths: fp4 3 (2 if tight), raw whatever is left (<= 4, >= 2)
+    for (int f4 = 3; f4 >= 2; --f4) {
+        const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
+        if (raw >= 2) {
+            g.f4_st = f4;
+            g.raw_st = raw < H7_MAX_ST ? raw : H7_MAX_ST;
+            g.ok = true;
+            return g;
+        }
+    }
+    return g;
+}
+}  // namespace
+
+// Whether K7 takes a conv: stride 1, padding that reads as 0 (ternary map or
+// no padding), 128-channel blocks, a padded row of <= 128 pixels, and a
+// filter + two raw and two fp4 halo stages that fit in shared memory.
+bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int kw, int stride, int pad,
+                       long long batch) {
+    if (!(pad == 0 || !fm_binary)) return false;
+    const HaloGeom g = halo_geom(h, w, c, cout, kh, kw, stride, pad);
+    if (!g.ok) return false;
+    const long long tpi = (h + 2 * pad - kh + 1 + g.R - 1) / g.R;
+    return batch * tpi < 0x7FFFFFFFLL;
+}
+
+lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int pad,
+                               int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
+                               int* zero_flag, cudaStream_t stream) {
+    const HaloGeom g = halo_geom(h, w, cch, cout, kh, kw, 1, pad);
+    if (!g.ok) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv halo kernel: unsupported shape");
+    const int oh = h + 2 * pad - kh + 1, ow = w + 2 * pad - kw + 1;
+    const int k = kh * kw * cch;
+    const WeightsLayout L(b_ternary, cout, k);
+    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
+
+    HaloParams prm{};
+    prm.batch = batch;
+    prm.h = h;
+    prm.w = w;
+    prm.oh = oh;
+    prm.ow = ow;
+    prm.pad = pad;
+    prm.kw = kw;
+    prm.cblocks = cch / 128;
+    prm.P = g.P;
+    prm.log2p = g.P == 32 ? 5 : (g.P == 64 ? 6 : 7);
+    prm.R = g.R;
+    prm.rows_h = g.rows_h;
+    prm.tpi = (oh + g.R - 1) / g.R;
+    prm.ctiles = batch * prm.tpi;
+    prm.ptiles = (prm.ctiles + 1) / 2;
+    prm.cout = cout;
+    prm.bn = g.bn;
+    prm.n_tiles = (cout + g.bn - 1) / g.bn;
+    prm.kblocks = g.kblocks;
+    prm.breg = g.breg;
+    prm.raw_cb = g.raw_cb;
+    prm.f4_cb = g.f4_cb;
+    prm.raw_st = g.raw_st;
+    prm.f4_st = g.f4_st;
+    prm.nacc = 3 * g.bn <= (int)H7_SF_COL ? 3 : 2;
+    prm.acc_cols = prm.nacc == 3 ? (int)H7_SF_COL / 3 : H7_MAX_BN;
+    prm.k33 = kh == 3 && kw == 3 && prm.cblocks == 1;
+    prm.check_zero = check_zero;
+    static const int dbg = getenv("LOWBIT_HALO_DEBUG") ? atoi(getenv("LOWBIT_HALO_DEBUG")) : 0;
+    prm.dbg = dbg;
+    prm.out = out;
+    prm.zero_flag = zero_flag;
+
+    CUtensorMap mb, mraw;
+    if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 64, (uint32_t)(g.bn / 2),
+                     CU_TENSOR_MAP_SWIZZLE_64B))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
+    if (!make_map_nhwc_box(&mraw, fm, batch, h, w, cch, (uint32_t)g.P, (uint32_t)g.rows_h))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the feature-map halo");
+    static bool attr = false;
+    if (!attr) {
+        LB_CUDA_TRY(cudaFuncSetAttribute(conv_fp4_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H7_SMEM));
+        attr = true;
+    }
+    const int pairs = prm.ptiles < num_sms() / 2 ? prm.ptiles : num_sms() / 2;
+    conv_fp4_halo_kernel<<<2 * pairs, H7_THREADS, H7_SMEM, stream>>>(mb, mraw, prm);
+    LB_CUDA_TRY(cudaGetLastError());
+    return LOWBIT_OK;
+}
+
+}  // namespace lb
+
+extern "C" int lowbit_debug_halo_trace(unsigned long long* out1024) {
+    return cudaMemcpyFromSymbol(out1024, lb::g_halo_trace, sizeof(unsigned long long) * 1024) != cudaSuccess;
+}

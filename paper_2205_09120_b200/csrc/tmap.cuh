@@ -53,6 +53,24 @@ inline bool make_map_conv_out(CUtensorMap* map, void* base, int batch, int oh, i
     return r == CUDA_SUCCESS;
 }
 
+// The NHWC int8 feature map [n, h, w, c] as a 4-D tiled map for boxes of
+// {128 channels, `pixels` pixels of a row, `rows` rows, 1 image}, no swizzle:
+// a box may start left of / above the image and run past its right / bottom
+// edge — those elements read as zero, which is the convolution's padding.
+inline bool make_map_nhwc_box(CUtensorMap* map, const void* base, int n, int h, int w, int c, uint32_t pixels,
+                              uint32_t rows) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)c, (cuuint64_t)w * c, (cuuint64_t)h * w * c};
+    cuuint32_t box[4] = {128, pixels, rows, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // 4-D NHWC int8 im2col map for implicit-GeMM convolution (fprop): lower
 // corner -pad, upper corner pad - (k-1), traversal stride = conv stride
 // (the CUTLASS convention, cutlass/conv/collective/detail.hpp).  Each load

@@ -105,7 +105,99 @@ void run(int n, int iters, int fill, int opts = 0) {
     cudaFree(d);
 }
 
-int main() {
+
+// The conv's operand shapes (K7): N = cout = 128, 64-byte-swizzled A/B rows
+// (SW64) vs 128-byte (SW128), one accumulator chain vs two interleaved.  All
+// descriptors precomputed; 4 MMAs per unrolled step so the issuing thread
+// never limits the rate.
+template <int SW64, int TWO_ACC>
+__global__ void __launch_bounds__(128, 1) conv_rate_kernel(int n, int iters, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    for (int i = threadIdx.x; i < 4 * 32768 / 4; i += blockDim.x) {
+        uint32_t h = (uint32_t)(i * 2654435761u) ^ (blockIdx.x * 0x9E3779B9u);
+        h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+        uint32_t w = 0;
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t r = (h >> (4 * j)) & 3;
+            w |= (r == 1 ? 0x2u : r == 2 ? 0xAu : 0u) << (4 * j);
+        }
+        reinterpret_cast<uint32_t*>(smem)[i] = w;
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __shared__ uint32_t tslot;
+    __shared__ uint64_t bar;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc_pair<512>(&tslot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tb = tslot;
+    {
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        for (uint32_t c = 448; c < 512; c += 16) tmem_st_32x32b_x16_fill(tb + lane_base + c, 0x7F7F7F7Fu);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (cluster_ctarank() == 0 && threadIdx.x == 0) {
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 65536);
+        const uint32_t id = idesc_mxf4(256, n);
+        uint64_t ad[4], bd[4];
+        for (int q = 0; q < 4; ++q) {
+            if (SW64) {  // K offset 0 / 32 bytes in 64-byte rows; A rows shifted by q (the halo taps)
+                const uint32_t ao = a + (q & 1) * 32 + q * 64, bo = b + (q & 1) * 32;
+                ad[q] = (uint64_t)((ao >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(512u >> 4) << 32) | (1ull << 46) | (4ull << 61);
+                bd[q] = (uint64_t)((bo >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(512u >> 4) << 32) | (1ull << 46) | (4ull << 61);
+            } else {
+                ad[q] = umma_desc_k_sw128(a + q * 32);
+                bd[q] = umma_desc_k_sw128(b + q * 32);
+            }
+        }
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                umma_mxf4_pair(tb + (TWO_ACC ? (uint32_t)(q & 1) * 224u : 0u), ad[q], bd[q], id, tb + 448, tb + 448, 1);
+        }
+        umma_commit_pair(&bar, 0x1);
+        mbar_wait(&bar, 0);
+        out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc_pair<512>(tb); }
+}
+
+template <int SW64, int TWO_ACC>
+void conv_run(int n, int iters) {
+    auto k = conv_rate_kernel<SW64, TWO_ACC>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    unsigned long long* d; cudaMalloc(&d, 148 * 8); cudaMemset(d, 0, 148 * 8);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = 148; cfg.blockDim = 128; cfg.dynamicSmemBytes = 131072;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, n, iters / 10, d);
+    cudaLaunchKernelEx(&cfg, k, n, iters, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[148]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    unsigned long long mx = 0;
+    for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("conv shape: mxf4 pair N=%d %s %s: %s %.1f cycles/MMA\n", n, SW64 ? "SW64 (rows shifted)" : "SW128", TWO_ACC ? "two accumulators" : "one accumulator",
+           cudaGetErrorString(err), (double)mx / iters);
+    cudaFree(d);
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1) {
+        for (int n : {128, 256}) { conv_run<0, 0>(n, 200000); conv_run<1, 0>(n, 200000); conv_run<0, 1>(n, 200000); conv_run<1, 1>(n, 200000); }
+        return 0;
+    }
     const int it = 200000;
     for (int opts : {0, 1, 2, 3}) run<1, 1>(256, it, 1, opts);
     for (int opts : {0, 3}) run<1, 1>(208, it, 1, opts);
