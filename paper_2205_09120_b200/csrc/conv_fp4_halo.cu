@@ -24,16 +24,17 @@
 //   * The filter (prepared weights, fp4 section, K-major) stays resident in
 //     shared memory; tcgen05.mma.cta_group::2.kind::mxf4.block_scale with
 //     unit scales and f32 accumulators (exact: |partial sums| <= k <= 32767).
-//   * The epilogue converts each accumulator lane (one output pixel) to
-//     int16 and stores it straight to global memory (no staging: shared
-//     memory bandwidth is the scarce resource here — the N = cout = 128
-//     MMAs read 6 KB of operands per CTA per 64 cycles, ~75% of it).
+//   * The epilogue: 8 warps, two per TMEM lane quarter, each draining half of
+//     every tile's columns; it reads its whole share of the accumulator
+//     (releasing it to the MMAs at once), converts to int16 into a 128-byte-
+//     swizzled staging box and TMA-stores 32 pixels x 64 columns, clipped at
+//     the image edges by the tensor map.
 //   * Encoding: +-1 activations become +-0.5 (e2m1 0x1 / 0x9 = the int8 byte
 //     AND 0x09), the filter stays +-1.0, and the epilogue doubles the exact
 //     half-integer sums.
 //
-// Warp roles per CTA (608 threads): 0-7 epilogue (warps 0-3 drain even
-// tiles, 4-7 odd ones, one warp per TMEM lane quarter), 8-15 converters, 16
+// Warp roles per CTA (608 threads): 0-7 epilogue (two warps per TMEM lane
+// quarter, each half of every tile's columns), 8-15 converters, 16
 // TMA producer (raw halo + filter), 17-18 UMMA issuers on alternate tiles
 // (leader CTA; warp 17 also owns TMEM).
 #include <cstdio>
@@ -54,6 +55,7 @@ constexpr int H7_MAX_BN = 240;    // cout per tile: accumulators + scales <= 512
 constexpr uint32_t H7_SF_COL = 480;
 constexpr int H7_SMEM = 227 * 1024;
 constexpr int H7_BAR_BYTES = 1024;  // barriers + the k-block offset table
+constexpr int H7_EPI_BYTES = 8 * 4096;  // epilogue staging: one 32-pixel x 64-column int16 box per warp
 constexpr int H7_MAX_KB = 96;       // k-blocks (taps x channel blocks) the offset table holds
 constexpr int H7_MAX_ST = 4;        // raw / fp4 ring depth cap
 constexpr int H7_RAW_MAX = 64 * 1024;
@@ -72,7 +74,7 @@ struct HaloParams {
     int check_zero;            // binary map: a 0 activation sets *zero_flag (core.cpp:23)
     int dbg;                   // timing experiments (LOWBIT_HALO_DEBUG): 1 no stores, 2 no MMAs, 4 no conversion,
                                // 64 epilogue ignores tmem_full, 128 epilogue drains nothing, 32 trace,
-                               // 2048 no tiles (setup + teardown only)
+                               // 512 no raw halo loads, 2048 no tiles (setup + teardown only)
     int16_t* out;
     int* zero_flag;
 };
@@ -116,6 +118,7 @@ LB_DEV void h7_wait(int dbg, uint64_t* bar, uint32_t parity) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     conv_fp4_halo_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_raw,
+                         const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
                          const HaloParams prm) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -124,7 +127,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     uint8_t* sB = smem;                                      // resident filter: kblocks x breg
     uint8_t* sRaw = sB + prm.kblocks * prm.breg;             // raw int8 halo ring
     uint8_t* sF4 = sRaw + prm.raw_st * raw_stage;            // fp4 halo ring (the UMMA A operand)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sF4 + prm.f4_st * f4_stage);
+    uint8_t* sEpi = sF4 + prm.f4_st * f4_stage;             // epilogue staging: 4 KB per epilogue warp
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + H7_EPI_BYTES);
     uint64_t* raw_full = bars;            // local: TMA landed the raw halo
     uint64_t* raw_empty = bars + 4;       // local: the converter warps are done with it
     uint64_t* a_full = bars + 8;          // leader: fp4 halos of both CTAs written (all converter warps)
@@ -132,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     uint64_t* b_full = bars + 16;         // leader: the filter of this n tile landed (both CTAs)
     uint64_t* b_empty = bars + 17;        // local: both issuers' MMAs done with the filter
     uint64_t* tmem_full = bars + 18;      // local (3): accumulator complete
-    uint64_t* tmem_empty = bars + 21;     // leader (3): the tile's 8 epilogue warps (4 per CTA) drained it
+    uint64_t* tmem_empty = bars + 21;     // leader (3): the 16 epilogue warps (8 per CTA) drained it
     uint64_t* sf_ready = bars + 24;       // leader: unit scales written (16 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
     uint32_t* kb_aoff = reinterpret_cast<uint32_t*>(bars + 32);  // k-block -> A row offset (16-byte units)
@@ -156,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
         mbar_init(b_empty, 2);
         for (int a = 0; a < 3; ++a) {
             mbar_init(&tmem_full[a], 1);
-            mbar_init(&tmem_empty[a], 8);
+            mbar_init(&tmem_empty[a], 16);
         }
         mbar_init(sf_ready, 16);
         fence_barrier_init();
@@ -164,6 +168,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     if (warp == H7_W_PROD && lane == 0) {
         tma_prefetch_desc(&tmap_raw);
         tma_prefetch_desc(&tmap_b);
+        tma_prefetch_desc(&tmap_c64);
+        tma_prefetch_desc(&tmap_c16);
     }
     if (warp == H7_W_MMA) {
         tmem_alloc_pair<512>(tmem_slot);
@@ -193,6 +199,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                     const uint32_t s = t % prm.raw_st;
                     h7_wait(prm.dbg, &raw_empty[s], ((t / prm.raw_st) & 1) ^ 1);
                     if (nt == 0) H7_TRACE(0, i);
+                    if (prm.dbg & 512) {  // timing experiment: no raw loads (stale halo)
+                        mbar_arrive(&raw_full[s]);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&raw_full[s], (uint32_t)raw_stage);
                     const int ct = (pair + i * npairs) * 2 + (int)rank;  // this CTA's tile
                     int img = ct / prm.tpi;
@@ -345,7 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     } else {
         // ===================== epilogue (both CTAs): warps 0-7 =====================
         const int wq = warp & 3;     // TMEM lane quarter = 32 output positions
-        const int half = warp >> 2;  // which warp group: even or odd tiles
+        const int half = warp >> 2;  // which half of the tile's columns
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         tmem_st_32x32b_x8_fill(tmem_base + lane_base + H7_SF_COL, 0x7F7F7F7Fu);  // unit UE8M0 scales
         tmem_st_wait();
@@ -353,28 +363,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(sf_ready), 0));
         const uint32_t tmem_empty0 = mapa_shared(smem_u32(&tmem_empty[0]), 0);
-        const int nch = bn / 16;
-        // The warp's 32 positions are 32 consecutive pixels of one output row
-        // (P is a multiple of 32); lane l holds pixel l's columns and stores
-        // them as 32-byte vectors (one full sector per lane).  Staging through
-        // shared memory for coalesced 128-byte rows (or an 8 x 8 shuffle
-        // transpose, which runs on the same crossbar) measured slower: shared
-        // memory bandwidth is the kernel's binding resource.
+        const int nch = bn / 16, nch0 = (nch + 1) / 2;
+        const int ch0 = half ? nch0 : 0, ch1 = half ? nch : nch0;  // this warp's 16-column chunks
+        // The warp's 32 positions are 32 consecutive pixels of one output row (P
+        // is a multiple of 32): one TMA store box of 32 pixels x 64 columns.
         const int ry = (wq * 32) / prm.P, ox0 = (wq * 32) % prm.P;
-        const bool v8ok = (prm.cout & 15) == 0;  // 32-byte aligned pixel rows
+        const uint32_t stg = smem_u32(sEpi) + (uint32_t)warp * 4096u;  // this warp's staging box
         int u = 0;
         for (int nt = 0; nt < prm.n_tiles; ++nt)
             for (int i = 0; i < my_tiles; ++i, ++u) {
-                if ((u & 1) != half) continue;  // the two warp groups drain alternate tiles
                 const int acc = u % prm.nacc;
                 const uint32_t acc_phase = (uint32_t)(u / prm.nacc) & 1;
                 const int ct = (pair + i * npairs) * 2 + (int)rank;
                 const int img = ct / prm.tpi;
                 const int oy = (ct - img * prm.tpi) * prm.R + ry;
-                const bool row_ok = ct < prm.ctiles && oy < prm.oh && !(prm.dbg & 1);
-                const bool col_ok0 = row_ok && ox0 + lane < prm.ow;  // this lane's pixel exists
-                int16_t* orow = prm.out + (((long long)img * prm.oh + oy) * prm.ow + ox0) * prm.cout + nt * bn;
-                const int cmax = prm.cout - nt * bn;  // valid columns of this n tile
+                const bool store_ok = ct < prm.ctiles && oy < prm.oh && !(prm.dbg & 1);
                 if (!(prm.dbg & 64)) h7_wait(prm.dbg, &tmem_full[acc], acc_phase);
                 tc_fence_after();
                 if (wq == 0 && lane == 0) H7_TRACE(7, u);
@@ -385,54 +388,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                     continue;
                 }
                 const uint32_t tacc = tmem_base + lane_base + (uint32_t)(acc * prm.acc_cols);
-                for (int g = 0; g < nch; g += 4) {
-                    const int nc = nch - g < 4 ? nch - g : 4;
-                    // unit q (16 bytes) = columns 16g + 8q .. +7 of this lane's pixel; the f32
-                    // sums are half-integers: 2x + 1.5*2^23 is exact and its low 16 bits are
-                    // the int16 result (see gemm_fp4_pair.cu)
+                // f32 sums are half-integers: 2x + 1.5*2^23 is exact and its low 16 bits are the
+                // int16 result (see gemm_fp4_pair.cu); 16 columns -> 8 packed words
+                auto pack16 = [](const uint32_t (&v)[16], uint32_t (&w8)[8]) {
 #pragma unroll
-                    for (int hc = 0; hc < 2; ++hc) {
-                        uint32_t v[2][16];
+                    for (int q = 0; q < 8; ++q)
+                        w8[q] = __byte_perm(__float_as_uint(fmaf(__uint_as_float(v[2 * q]), 2.0f, 12582912.0f)),
+                                            __float_as_uint(fmaf(__uint_as_float(v[2 * q + 1]), 2.0f, 12582912.0f)),
+                                            0x5410);
+                };
+                auto release = [&]() {  // the tile's last TMEM read is done: hand the accumulator back
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
+                    if (wq == 0 && lane == 0) H7_TRACE(8, u);
+                };
+                // Groups of up to 4 chunks (64 columns) go through this warp's 4 KB staging box
+                // (128-byte swizzle; 16-column boxes with 32-byte swizzle for a tail) and out by
+                // TMA store: 32 pixels x 64 columns per instruction, clipped at the image's
+                // right / bottom edge by the tensor map.  Direct per-lane 32-byte stores cost 32
+                // L1 lines per instruction and their stalls delayed the accumulator's release.
+                for (int g = ch0; g < ch1; g += 4) {
+                    const int nc = ch1 - g < 4 ? ch1 - g : 4;
+                    if (lane == 0) bulk_wait_read<0>();  // the previous box left the staging buffer
+                    __syncwarp();
 #pragma unroll
-                        for (int c = 0; c < 2; ++c)
-                            if (2 * hc + c < nc) tmem_ld_32x32b_x16(tacc + (g + 2 * hc + c) * 16, v[c]);
+                    for (int c = 0; c < 4; ++c) {
+                        if (c >= nc) break;
+                        uint32_t v[16], w8[8];
+                        tmem_ld_32x32b_x16(tacc + (g + c) * 16, v);
                         tmem_ld_wait();
-                        if (wq == 0 && lane == 0 && g == 0) H7_TRACE(10 + 2 * hc, u);
-                        if (hc == 1 && g + 4 >= nch) {  // the tile's last TMEM read: hand the accumulator back
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
-                            if (wq == 0 && lane == 0) H7_TRACE(8, u);
+                        if (c == nc - 1 && g + 4 >= ch1) release();
+                        pack16(v, w8);
+                        if (nc == 4) {  // SW128: 16-byte unit q of row `lane` at ((q ^ (lane & 7)) << 4)
+                            const uint32_t row = stg + lane * 128;
+                            sts_v4(row + (((2 * c) ^ (lane & 7)) << 4), w8[0], w8[1], w8[2], w8[3]);
+                            sts_v4(row + (((2 * c + 1) ^ (lane & 7)) << 4), w8[4], w8[5], w8[6], w8[7]);
+                        } else {        // SW32 1 KB boxes
+                            const uint32_t row = stg + c * 1024 + lane * 32;
+                            const uint32_t sw = (uint32_t)(lane >> 2) & 1;
+                            sts_v4(row + (sw << 4), w8[0], w8[1], w8[2], w8[3]);
+                            sts_v4(row + ((sw ^ 1) << 4), w8[4], w8[5], w8[6], w8[7]);
                         }
-#pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            if (2 * hc + c >= nc) break;
-                            uint32_t w8[8];
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                w8[q] = __byte_perm(
-                                    __float_as_uint(fmaf(__uint_as_float(v[c][2 * q]), 2.0f, 12582912.0f)),
-                                    __float_as_uint(fmaf(__uint_as_float(v[c][2 * q + 1]), 2.0f, 12582912.0f)),
-                                    0x5410);
-                            // direct 32-byte stores (one full sector per lane): no shared-memory
-                            // traffic, which the MMA operand reads need (smem-bandwidth bound)
-                            const int col = (g + 2 * hc + c) * 16;
-                            if (col_ok0 && col < cmax) {
-                                int16_t* dst = orow + (long long)lane * prm.cout + col;
-                                if (v8ok && col + 16 <= cmax) {
-                                    stg_v8(dst, w8);
-                                } else {
-                                    stg_v4(dst, w8[0], w8[1], w8[2], w8[3]);
-                                    if (col + 8 < cmax) stg_v4(dst + 8, w8[4], w8[5], w8[6], w8[7]);
-                                }
-                            }
-                        }
-                        if (wq == 0 && lane == 0 && g == 0) H7_TRACE(11 + 2 * hc, u);
                     }
-                    if (wq == 0 && lane == 0 && g == 0) H7_TRACE(14, u);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && store_ok) {
+                        const int col = nt * bn + g * 16;
+                        if (nc == 4) tma_store_4d(&tmap_c64, stg, col, ox0, oy, img);
+                        else
+                            for (int c = 0; c < nc; ++c) tma_store_4d(&tmap_c16, stg + c * 1024, col + c * 16, ox0, oy, img);
+                        bulk_commit();
+                    }
                 }
                 if (wq == 0 && lane == 0) H7_TRACE(9, u);
             }
+        if (lane == 0) bulk_wait<0>();
     }
 
     tc_fence_before();
@@ -472,7 +483,7 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
     g.raw_cb = g.rows_h * g.P * 128;
     g.f4_cb = ((g.rows_h * g.P + 8) * 64 + 1023) / 1024 * 1024;  // + the taps' over-read past the halo
     if (g.kblocks > H7_MAX_KB || cb * g.raw_cb > H7_RAW_MAX) return g;
-    const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - g.kblocks * g.breg;
+    const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - H7_EPI_BYTES - g.kblocks * g.breg;
     // ring depths: fp4 3 (2 if tight), raw whatever is left (<= 4, >= 2)
     for (int f4 = 3; f4 >= 2; --f4) {
         const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
@@ -543,7 +554,9 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     prm.out = out;
     prm.zero_flag = zero_flag;
 
-    CUtensorMap mb, mraw;
+    CUtensorMap mb, mraw, mc64, mc16;
+    if (!make_map_conv_out(&mc64, out, batch, oh, ow, cout, 64) || !make_map_conv_out(&mc16, out, batch, oh, ow, cout, 16))
+        return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv output");
     if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 64, (uint32_t)(g.bn / 2),
                      CU_TENSOR_MAP_SWIZZLE_64B))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
@@ -555,7 +568,7 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
         attr = true;
     }
     const int pairs = prm.ptiles < num_sms() / 2 ? prm.ptiles : num_sms() / 2;
-    conv_fp4_halo_kernel<<<2 * pairs, H7_THREADS, H7_SMEM, stream>>>(mb, mraw, prm);
+    conv_fp4_halo_kernel<<<2 * pairs, H7_THREADS, H7_SMEM, stream>>>(mb, mraw, mc64, mc16, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

@@ -26,3 +26,12 @@ for i in range(8):
 print("converter warp 0: a_empty -> converted, -> fenced")
 for i in range(8):
     print(i, [ev[15][i] - ev[2][i], ev[3][i] - ev[15][i]])
+def avg(xs):
+    xs = [x for x in xs if x > -10**12]
+    return sum(xs) / max(len(xs), 1)
+T = range(4, 12)
+print("steady state (tiles 4-11): producer period %.0f, raw latency issue->converter %.0f, converter busy %.0f, "
+      "MMA issue span %.0f, MMA period %.0f, epilogue span %.0f" % (
+          avg([ev[0][i + 1] - ev[0][i] for i in T]), avg([ev[1][i] - ev[0][i] for i in T]),
+          avg([ev[3][i] - ev[2][i] for i in T]), avg([ev[6][i] - ev[5][i] for i in T]),
+          avg([ev[6][i + 1] - ev[6][i] for i in T]), avg([ev[9][i] - ev[7][i] for i in T])))
