@@ -73,8 +73,9 @@ struct HaloParams {
     int k33;                   // 3x3 filter over one channel block: the unrolled issue loop
     int check_zero;            // binary map: a 0 activation sets *zero_flag (core.cpp:23)
     int dbg;                   // timing experiments (LOWBIT_HALO_DEBUG): 1 no stores, 2 no MMAs, 4 no conversion,
+                               // 8 no TMEM loads, 16 no staging stores,
                                // 64 epilogue ignores tmem_full, 128 epilogue drains nothing, 32 trace,
-                               // 512 no raw halo loads, 2048 no tiles (setup + teardown only)
+                               // 512 no raw halo loads, 2048 no tiles (setup + teardown only), 4096 one MMA issuer
     int16_t* out;
     int* zero_flag;
 };
@@ -300,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
             const uint64_t bd0 = h7_desc_sw64(smem_u32(sB));
             const uint32_t p4 = (uint32_t)prm.P * 4;  // one halo row of positions in 16-byte units
             const bool skip_mma = (prm.dbg & 2) != 0;
-            const bool kx_off = !(prm.dbg & 8);  // timing experiment: 8-row-aligned A for every tap (wrong results)
+            const bool single = (prm.dbg & 4096) != 0;      // timing experiment: one issuer for all tiles
             mbar_wait(sf_ready, 0);
             tc_fence_after();
             uint32_t t = 0;
@@ -312,7 +313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                     const int u = (int)t;
                     const int a = acc;
                     if (++acc == prm.nacc) acc = 0;
-                    if ((u & 1) != which) continue;  // the other issuer's tile
+                    if (single ? which != 0 : (u & 1) != which) continue;  // the other issuer's tile
                     mbar_wait_poll(&tmem_empty[a], ((uint32_t)(u / prm.nacc) & 1) ^ 1);
                     if (lane == 0) H7_TRACE(4, t);
                     const uint32_t fs = t % prm.f4_st;
@@ -325,7 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                         if (prm.k33) {
 #pragma unroll
                             for (int kb = 0; kb < 9; ++kb) {
-                                const uint64_t ad = ad0 + (uint32_t)((kb / 3) * p4 + (kx_off ? (kb % 3) * 4 : 0));
+                                const uint64_t ad = ad0 + (uint32_t)((kb / 3) * p4 + (kb % 3) * 4);
                                 const uint64_t bd = bd0 + (uint32_t)(kb * breg16);
                                 if (!skip_mma || kb == 0) {
                                     umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
@@ -416,11 +417,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                     for (int c = 0; c < 4; ++c) {
                         if (c >= nc) break;
                         uint32_t v[16], w8[8];
-                        tmem_ld_32x32b_x16(tacc + (g + c) * 16, v);
-                        tmem_ld_wait();
+                        if (!(prm.dbg & 8)) {
+                            tmem_ld_32x32b_x16(tacc + (g + c) * 16, v);
+                            tmem_ld_wait();
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) v[q] = (uint32_t)q;
+                        }
                         if (c == nc - 1 && g + 4 >= ch1) release();
                         pack16(v, w8);
-                        if (nc == 4) {  // SW128: 16-byte unit q of row `lane` at ((q ^ (lane & 7)) << 4)
+                        if (prm.dbg & 16) {  // timing experiment: no staging stores
+                        } else if (nc == 4) {  // SW128: 16-byte unit q of row `lane` at ((q ^ (lane & 7)) << 4)
                             const uint32_t row = stg + lane * 128;
                             sts_v4(row + (((2 * c) ^ (lane & 7)) << 4), w8[0], w8[1], w8[2], w8[3]);
                             sts_v4(row + (((2 * c + 1) ^ (lane & 7)) << 4), w8[4], w8[5], w8[6], w8[7]);
