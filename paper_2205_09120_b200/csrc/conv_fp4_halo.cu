@@ -75,7 +75,8 @@ struct HaloParams {
     int dbg;                   // timing experiments (LOWBIT_HALO_DEBUG): 1 no stores, 2 no MMAs, 4 no conversion,
                                // 8 no TMEM loads, 16 no staging stores,
                                // 64 epilogue ignores tmem_full, 128 epilogue drains nothing, 32 trace,
-                               // 512 no raw halo loads, 2048 no tiles (setup + teardown only), 4096 one MMA issuer
+                               // 512 no raw halo loads, 2048 no tiles (setup + teardown only), 4096 one MMA issuer,
+                               // 32768 return at entry (launch cost)
     int16_t* out;
     int* zero_flag;
 };
@@ -121,6 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     conv_fp4_halo_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_raw,
                          const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
                          const HaloParams prm) {
+    if (prm.dbg & 32768) return;  // launch-overhead probe
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int CB = prm.cblocks;
