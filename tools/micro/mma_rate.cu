@@ -110,7 +110,7 @@ void run(int n, int iters, int fill, int opts = 0) {
 // (SW64) vs 128-byte (SW128), one accumulator chain vs two interleaved.  All
 // descriptors precomputed; 4 MMAs per unrolled step so the issuing thread
 // never limits the rate.
-template <int SW64, int TWO_ACC, int BG = 0>
+template <int SW64, int TWO_ACC, int BG = 0, int LDCOL = 256>
 __global__ void __launch_bounds__(384, 1) conv_rate_kernel(int n, int iters, unsigned long long* out,
                                                            uint4* gbuf) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -163,10 +163,25 @@ __global__ void __launch_bounds__(384, 1) conv_rate_kernel(int n, int iters, uns
                 const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    tmem_ld_32x32b_x16(tb + lane_base + 256 + ((it * 4 + q) & 7) * 16, v);
+                    tmem_ld_32x32b_x16(tb + lane_base + (uint32_t)LDCOL + ((it * 4 + q) & 7) * 16, v);
                     tmem_ld_wait();
                     acc.x ^= v[0] + v[15];
                 }
+            } else if (BG == 4 || BG == 5) {  // shared stores + proxy fence (4), or the fence alone (5)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (BG == 4) sts_v4(base + 4096 * 4 + (q & 3) * 512, acc.x, acc.y, (uint32_t)it, (uint32_t)q);
+                    fence_proxy_async_smem();
+                }
+                acc.x += 1;
+            } else if (BG == 6) {  // tcgen05.fence::before_thread_sync / after, as the epilogue's handshakes
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    tc_fence_before();
+                    __syncwarp();
+                    tc_fence_after();
+                }
+                acc.x += 1;
             } else if (BG == 2) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -217,9 +232,9 @@ __global__ void __launch_bounds__(384, 1) conv_rate_kernel(int n, int iters, uns
     if (warp == 0) { tc_fence_after(); tmem_dealloc_pair<512>(tb); }
 }
 
-template <int SW64, int TWO_ACC, int BG = 0>
+template <int SW64, int TWO_ACC, int BG = 0, int LDCOL = 256>
 void conv_run(int n, int iters) {
-    auto k = conv_rate_kernel<SW64, TWO_ACC, BG>;
+    auto k = conv_rate_kernel<SW64, TWO_ACC, BG, LDCOL>;
     static uint4* gbuf = nullptr;
     if (!gbuf) cudaMalloc(&gbuf, (size_t)148 * 8 * 32 * 64 * 16 * 2);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
@@ -237,17 +252,101 @@ void conv_run(int n, int iters) {
     unsigned long long h[148]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
     unsigned long long mx = 0;
     for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-    printf("conv shape: mxf4 pair N=%d %s %s, background %s: %s %.1f cycles/MMA\n", n, SW64 ? "SW64 (rows shifted)" : "SW128",
-           TWO_ACC == 1 ? "two accumulators" : TWO_ACC == 2 ? "accumulator at column 160" : TWO_ACC == 3 ? "accumulator at column 320" : "one accumulator", BG == 0 ? "none" : BG == 1 ? "LDS.128+STS.128 x8 warps" : BG == 2 ? "STG.256 x8 warps" : "tcgen05.ld x8 warps",
+    printf("conv shape (ld col %d): mxf4 pair N=%d %s %s, background %s: %s %.1f cycles/MMA\n", LDCOL, n, SW64 ? "SW64 (rows shifted)" : "SW128",
+           TWO_ACC == 1 ? "two accumulators" : TWO_ACC == 2 ? "accumulator at column 160" : TWO_ACC == 3 ? "accumulator at column 320" : "one accumulator", BG == 0 ? "none" : BG == 1 ? "LDS.128+STS.128 x8 warps" : BG == 2 ? "STG.256 x8 warps" : BG == 3 ? "tcgen05.ld x8 warps" : BG == 4 ? "STS + fence.proxy.async x8 warps" : BG == 5 ? "fence.proxy.async x8 warps" : "tcgen05 fences x8 warps",
            cudaGetErrorString(err), (double)mx / iters);
     cudaFree(d);
 }
 
+// The conv kernel's MMA-side pipeline without its data: tiles of 18 MMAs
+// (the first with accumulate = 0) on a ring of NACC accumulators, one commit
+// per tile, NISS issuing warps on alternate tiles, each waiting for the
+// commit of the tile NACC back before reusing its accumulator.
+template <int NISS, int NACC>
+__global__ void __launch_bounds__(128, 1) conv_pipe_kernel(int tiles, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    for (int i = threadIdx.x; i < 4 * 32768 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x22A022A0u ^ (i * 0x01010101u & 0x08080808u);
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __shared__ uint32_t tslot;
+    __shared__ uint64_t full[4];
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { for (int a = 0; a < 4; ++a) mbar_init(&full[a], 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc_pair<512>(&tslot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tb = tslot;
+    {
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        tmem_st_32x32b_x8_fill(tb + lane_base + 480, 0x7F7F7F7Fu);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (cluster_ctarank() == 0 && warp < NISS && (threadIdx.x & 31) == 0) {
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 65536);
+        const uint32_t id = idesc_mxf4(256, 128);
+        auto desc = [](uint32_t o) {
+            return (uint64_t)((o >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(512u >> 4) << 32) | (1ull << 46) | (4ull << 61);
+        };
+        const uint64_t ad0 = desc(a), bd0 = desc(b);
+        const long long t0 = clock64();
+        for (int t = warp; t < tiles; t += NISS) {
+            const int acc = t % NACC;
+            if (t >= NACC) mbar_wait(&full[acc], ((t / NACC) - 1) & 1);
+            tc_fence_after();
+            const uint32_t d = tb + (uint32_t)acc * 160u;
+#pragma unroll
+            for (int kb = 0; kb < 9; ++kb) {
+                const uint64_t ad = ad0 + (uint32_t)((kb / 3) * 256 + (kb % 3) * 4), bd = bd0 + (uint32_t)kb * 256;
+                umma_mxf4_pair(d, ad, bd, id, tb + 480, tb + 480, kb != 0);
+                umma_mxf4_pair(d, ad + 2, bd + 2, id, tb + 480, tb + 480, 1);
+            }
+            umma_commit_pair(&full[acc], 0x1);
+        }
+        // drain: wait for this issuer's last tile
+        int last = warp;
+        while (last + NISS < tiles) last += NISS;
+        mbar_wait(&full[last % NACC], (last / NACC) & 1);
+        out[blockIdx.x * 2 + warp] = (unsigned long long)(clock64() - t0);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc_pair<512>(tb); }
+}
+
+template <int NISS, int NACC>
+void pipe_run(int tiles) {
+    auto k = conv_pipe_kernel<NISS, NACC>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    unsigned long long* d; cudaMalloc(&d, 148 * 16); cudaMemset(d, 0, 148 * 16);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = 148; cfg.blockDim = 128; cfg.dynamicSmemBytes = 131072;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, tiles, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[296]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    unsigned long long mx = 0;
+    for (int i = 0; i < 296; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("conv pipe: %d issuer(s), %d accumulators, %d tiles of 18 MMAs: %s %.1f cycles per tile (%.1f per MMA)\n", NISS, NACC,
+           tiles, cudaGetErrorString(err), (double)mx / tiles, (double)mx / tiles / 18);
+    cudaFree(d);
+}
+
 int main(int argc, char** argv) {
+    if (argc > 2) {
+        pipe_run<1, 3>(2000); pipe_run<2, 3>(2000); pipe_run<1, 2>(2000); pipe_run<2, 2>(2000);
+        return 0;
+    }
     if (argc > 1) {
         conv_run<1, 0, 0>(128, 200000); conv_run<1, 0, 1>(128, 200000); conv_run<1, 0, 2>(128, 200000);
         conv_run<1, 0, 3>(128, 200000);
-        conv_run<1, 2, 0>(128, 200000); conv_run<1, 3, 0>(128, 200000);
+        conv_run<1, 0, 3, 0>(128, 200000); conv_run<1, 0, 3, 128>(128, 200000); conv_run<1, 0, 3, 160>(128, 200000);
         return 0;
     }
     const int it = 200000;
