@@ -83,6 +83,14 @@ struct HaloParams {
 
 // dbg & 32: per-tile event times (clock64) of pair 0's leader CTA, read by lowbit_debug_halo_trace
 __device__ unsigned long long g_halo_trace[16 * 64];
+// dbg & 32: kernel phases in %globaltimer ns over all CTAs: first entry, last end of setup,
+// last end of work, last exit
+__device__ unsigned long long g_halo_phase[4];
+LB_DEV unsigned long long h7_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #define H7_TRACE(ev, i) \
     if ((prm.dbg & 32) && pair == 0 && leader && (i) < 64) g_halo_trace[(ev) * 64 + (i)] = clock64()
 
@@ -123,6 +131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                          const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
                          const HaloParams prm) {
     if (prm.dbg & 32768) return;  // launch-overhead probe
+    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMin(&g_halo_phase[0], h7_gtime());
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int CB = prm.cblocks;
@@ -186,6 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[1], h7_gtime());
 
     if (warp == H7_W_PROD) {
         // ===================== TMA producer (both CTAs): filter + raw halos =====================
@@ -457,11 +467,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
 
     tc_fence_before();
     __syncthreads();
+    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[2], h7_gtime());
     cluster_sync();
     if (warp == H7_W_MMA) {
         tc_fence_after();
         tmem_dealloc_pair<512>(tmem_base);
     }
+    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[3], h7_gtime());
 }
 
 static int h7_pick_bn(int cout) {
@@ -586,4 +598,13 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
 
 extern "C" int lowbit_debug_halo_trace(unsigned long long* out1024) {
     return cudaMemcpyFromSymbol(out1024, lb::g_halo_trace, sizeof(unsigned long long) * 1024) != cudaSuccess;
+}
+// phases of the last K7 launch with LOWBIT_HALO_DEBUG & 32 (ns); reset = 1 re-arms them
+extern "C" int lowbit_debug_halo_phases(unsigned long long* out4, int reset) {
+    if (cudaMemcpyFromSymbol(out4, lb::g_halo_phase, sizeof(unsigned long long) * 4) != cudaSuccess) return 1;
+    if (reset) {
+        const unsigned long long init[4] = {~0ull, 0, 0, 0};
+        return cudaMemcpyToSymbol(lb::g_halo_phase, init, sizeof init) != cudaSuccess;
+    }
+    return 0;
 }

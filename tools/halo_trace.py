@@ -11,6 +11,13 @@ o = torch.empty((64, 56, 56, 128), dtype=torch.int16, device="cuda")
 for _ in range(3):
     lb.conv2d_lowbit(1, fm, False, w, 3, 3, 1, 1, kernel=2, out=o)
 torch.cuda.synchronize()
+ph = (C.c_ulonglong * 4)()
+lb._lib.lib.lowbit_debug_halo_phases(ph, 1)
+lb.conv2d_lowbit(1, fm, False, w, 3, 3, 1, 1, kernel=2, out=o)
+torch.cuda.synchronize()
+assert lb._lib.lib.lowbit_debug_halo_phases(ph, 0) == 0
+print("phases (us): first entry -> last setup end %.2f, -> last work end %.2f, -> last exit %.2f (total %.2f)" % (
+    (ph[1] - ph[0]) / 1e3, (ph[2] - ph[1]) / 1e3, (ph[3] - ph[2]) / 1e3, (ph[3] - ph[0]) / 1e3))
 buf = (C.c_ulonglong * 1024)()
 assert lb._lib.lib.lowbit_debug_halo_trace(buf) == 0
 ev = [[buf[e * 64 + i] for i in range(64)] for e in range(16)]

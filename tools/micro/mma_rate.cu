@@ -146,7 +146,26 @@ __global__ void __launch_bounds__(384, 1) conv_rate_kernel(int n, int iters, uns
     __shared__ volatile int done;
     if (threadIdx.x == 0) done = 0;
     __syncthreads();
-    if (BG && warp >= 4) {  // background traffic from 8 warps while the MMAs run
+    if (BG == 7) {  // background TMA (bulk) writes into shared memory: warp 4 lane 0, 4 x 8 KB copies in flight
+        if (warp == 4 && (threadIdx.x & 31) == 0) {
+            __shared__ uint64_t tbar[4];
+            for (int q = 0; q < 4; ++q) mbar_init(&tbar[q], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const uint32_t dst0 = smem_u32(smem + 98304);
+            uint32_t n[4] = {0, 0, 0, 0};  // copies issued per slot; copy k of a slot completes phase k
+            for (int it = 0; !done; ++it) {
+                const int q = it & 3;
+                if (n[q]) mbar_wait(&tbar[q], (n[q] - 1) & 1);
+                mbar_arrive_expect_tx(&tbar[q], 8192);
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                                 "r"(dst0 + q * 8192), "l"(reinterpret_cast<const uint8_t*>(gbuf) + (size_t)((blockIdx.x * 64 + (it & 63)) & 8191) * 8192),
+                             "r"(8192), "r"(smem_u32(&tbar[q])) : "memory");
+                ++n[q];
+            }
+            for (int q = 0; q < 4; ++q)
+                if (n[q]) mbar_wait(&tbar[q], (n[q] - 1) & 1);
+        }
+    } else if (BG && warp >= 4) {  // background traffic from 8 warps while the MMAs run
         const uint32_t base = smem_u32(smem + 98304) + (warp - 4) * 2048 + (threadIdx.x & 31) * 16;
         uint4 acc = make_uint4(0, 0, 0, 0);
         uint4* g = gbuf + ((size_t)blockIdx.x * 8 + (warp - 4)) * 32 * 64 + (threadIdx.x & 31) * 2;
@@ -236,7 +255,7 @@ template <int SW64, int TWO_ACC, int BG = 0, int LDCOL = 256>
 void conv_run(int n, int iters) {
     auto k = conv_rate_kernel<SW64, TWO_ACC, BG, LDCOL>;
     static uint4* gbuf = nullptr;
-    if (!gbuf) cudaMalloc(&gbuf, (size_t)148 * 8 * 32 * 64 * 16 * 2);
+    if (!gbuf) cudaMalloc(&gbuf, (size_t)8192 * 8192 + 4096);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
     unsigned long long* d; cudaMalloc(&d, 148 * 8); cudaMemset(d, 0, 148 * 8);
     cudaLaunchConfig_t cfg = {};
@@ -253,7 +272,7 @@ void conv_run(int n, int iters) {
     unsigned long long mx = 0;
     for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
     printf("conv shape (ld col %d): mxf4 pair N=%d %s %s, background %s: %s %.1f cycles/MMA\n", LDCOL, n, SW64 ? "SW64 (rows shifted)" : "SW128",
-           TWO_ACC == 1 ? "two accumulators" : TWO_ACC == 2 ? "accumulator at column 160" : TWO_ACC == 3 ? "accumulator at column 320" : "one accumulator", BG == 0 ? "none" : BG == 1 ? "LDS.128+STS.128 x8 warps" : BG == 2 ? "STG.256 x8 warps" : BG == 3 ? "tcgen05.ld x8 warps" : BG == 4 ? "STS + fence.proxy.async x8 warps" : BG == 5 ? "fence.proxy.async x8 warps" : "tcgen05 fences x8 warps",
+           TWO_ACC == 1 ? "two accumulators" : TWO_ACC == 2 ? "accumulator at column 160" : TWO_ACC == 3 ? "accumulator at column 320" : "one accumulator", BG == 0 ? "none" : BG == 1 ? "LDS.128+STS.128 x8 warps" : BG == 2 ? "STG.256 x8 warps" : BG == 3 ? "tcgen05.ld x8 warps" : BG == 4 ? "STS + fence.proxy.async x8 warps" : BG == 5 ? "fence.proxy.async x8 warps" : BG == 7 ? "bulk TMA writes 4 x 8 KB in flight" : "tcgen05 fences x8 warps",
            cudaGetErrorString(err), (double)mx / iters);
     cudaFree(d);
 }
@@ -338,7 +357,91 @@ void pipe_run(int tiles) {
     cudaFree(d);
 }
 
+// K5's issue pattern: stages of 8 pair MMAs (N = 256, one accumulator chain),
+// an mbarrier wait (already complete) + a commit per stage; NISS issuing
+// warps take alternate stages, handing over through a shared-memory turn
+// counter so the chain stays in order.
+template <int NISS>
+__global__ void __launch_bounds__(128, 1) k5_pipe_kernel(int stages, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    for (int i = threadIdx.x; i < 4 * 32768 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x22A022A0u ^ (i * 0x01010101u & 0x08080808u);
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __shared__ uint32_t tslot;
+    __shared__ uint64_t ready, done;
+    __shared__ volatile uint32_t turn;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { mbar_init(&ready, 1); mbar_init(&done, 1); turn = 0; fence_barrier_init(); }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive(&ready);  // phase 0 complete: every wait below succeeds at once
+    if (warp == 0) tmem_alloc_pair<512>(&tslot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tb = tslot;
+    {
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        tmem_st_32x32b_x8_fill(tb + lane_base + 256 + 248, 0x7F7F7F7Fu);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (cluster_ctarank() == 0 && warp < NISS && (threadIdx.x & 31) == 0) {
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 65536);
+        const uint32_t id = idesc_mxf4(256, 256);
+        const long long t0 = clock64();
+        for (int st = warp; st < stages; st += NISS) {
+            mbar_wait(&ready, 0);
+            tc_fence_after();
+            if (NISS > 1)
+                while (turn != (uint32_t)st) {
+                }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                umma_mxf4_pair(tb, umma_desc_k_sw128(a + (j & 3) * 32 + (j >> 2) * 16384),
+                               umma_desc_k_sw128(b + (j & 3) * 32 + (j >> 2) * 16384), id, tb + 504, tb + 504, st | j);
+            umma_commit_pair(&done, 0x1);
+            if (NISS > 1) turn = (uint32_t)st + 1;
+        }
+        if (warp == 0) {
+            while (turn != (uint32_t)stages && NISS > 1) {
+            }
+            umma_commit_pair(&ready, 0x1);  // (one more phase on a barrier nobody waits on afterwards)
+        }
+        out[blockIdx.x * 2 + warp] = (unsigned long long)(clock64() - t0);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc_pair<512>(tb); }
+}
+
+template <int NISS>
+void k5_pipe_run(int stages) {
+    auto k = k5_pipe_kernel<NISS>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    unsigned long long* d; cudaMalloc(&d, 148 * 16); cudaMemset(d, 0, 148 * 16);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = 148; cfg.blockDim = 128; cfg.dynamicSmemBytes = 131072;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, stages, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[296]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    unsigned long long mx = 0;
+    for (int i = 0; i < 296; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("K5 pattern: %d issuer(s), %d stages of 8 N=256 MMAs, a wait + commit per stage: %s %.1f cycles per MMA\n",
+           NISS, stages, cudaGetErrorString(err), (double)mx / stages / 8);
+    cudaFree(d);
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == 'k') {
+        k5_pipe_run<1>(4000); k5_pipe_run<2>(4000);
+        return 0;
+    }
     if (argc > 2) {
         pipe_run<1, 3>(2000); pipe_run<2, 3>(2000); pipe_run<1, 2>(2000); pipe_run<2, 2>(2000);
         return 0;
@@ -346,7 +449,7 @@ int main(int argc, char** argv) {
     if (argc > 1) {
         conv_run<1, 0, 0>(128, 200000); conv_run<1, 0, 1>(128, 200000); conv_run<1, 0, 2>(128, 200000);
         conv_run<1, 0, 3>(128, 200000);
-        conv_run<1, 0, 3, 0>(128, 200000); conv_run<1, 0, 3, 128>(128, 200000); conv_run<1, 0, 3, 160>(128, 200000);
+        conv_run<1, 0, 7>(128, 200000);
         return 0;
     }
     const int it = 200000;
