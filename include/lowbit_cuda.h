@@ -207,11 +207,24 @@ lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t
  * into out = int16 NHWC [batch][OH][OW][cout].  fm_binary is the feature
  * map's Mode (binary maps pad with binary_pad_value, ternary maps with 0);
  * a 0 in the A operand of a BNN conv sets *zero_flag.
- * TNN/TBN convs whose padding reads as 0 and whose c is a multiple of 128
- * run as an implicit GeMM: an im2col TMA map feeds the int8 activations
- * (values in {-1,0,+1}, the FeatureMap contract) straight to the tensor
- * cores, workspace unused.  Other convs go through lowbit_conv_encode. */
+ * Convs whose padding reads as 0 (ternary maps, or no padding) and whose c
+ * is a multiple of 128 run on the tensor cores straight from the int8 map
+ * (values in {-1,0,+1}, the FeatureMap contract): K7, a fused halo
+ * convolution (stride 1, padded rows of <= 128 pixels), else K6 (fp4
+ * implicit GeMM, uses the workspace), else an int8 implicit GeMM;
+ * lowbit_conv_select names the path.  Other convs go through
+ * lowbit_conv_encode. */
 long long lowbit_conv_rows(int batch, int h, int w, int kh, int kw, int stride, int padding);
+/* Which kernel lowbit_conv2d takes for a conv (host logic, no device needed;
+ * `kernel` as for lowbit_conv2d, has_workspace: a workspace will be passed). */
+enum {
+    LOWBIT_CONV_PATH_ENCODE_GEMM = 1, /* K4 fused im2col + encode, then lowbit_gemm */
+    LOWBIT_CONV_PATH_IMPLICIT_I8 = 3, /* TMA im2col over the int8 map -> tcgen05 kind::i8 */
+    LOWBIT_CONV_PATH_IMPLICIT_FP4 = 6, /* K6: packed fp4 map + TMA im2col -> kind::mxf4 */
+    LOWBIT_CONV_PATH_HALO_FP4 = 7     /* K7: fused halo convolution, one launch, no workspace */
+};
+int lowbit_conv_select(int mode, int fm_binary, int batch, int h, int w, int c, int cout, int kh, int kw, int stride,
+                       int padding, int kernel, int has_workspace);
 lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int batch, int h, int w, int c, int kh, int kw,
                                  int stride, int padding, int pad_value, uint8_t* plane0, uint8_t* plane1,
                                  long long pitch, int* zero_flag, lowbit_stream stream);
@@ -251,6 +264,10 @@ int lowbit_debug_pair_stats(unsigned long long* out16);
 int lowbit_debug_fp4_stats(unsigned long long* out16);
 /* Tuning aid: per-tile event clocks of K6's first leader CTA (LOWBIT_CONV_DEBUG & 32); 0 on success. */
 int lowbit_debug_conv_trace(unsigned long long* out1024);
+/* K7 timing experiments (LOWBIT_HALO_DEBUG & 32): per-tile clock64 events of
+ * pair 0's leader CTA, and kernel phases in globaltimer ns (reset re-arms). */
+int lowbit_debug_halo_trace(unsigned long long* out1024);
+int lowbit_debug_halo_phases(unsigned long long* out4, int reset);
 
 #ifdef __cplusplus
 }

@@ -19,4 +19,5 @@ from ._lib import (  # noqa: F401
 from .api import (  # noqa: F401
     Planes, PackedB, Weights, encode_binary, encode_ternary, pack_b, prepare_weights, gemm_lowbit,
     gemm_lowbit_host, generate, plane_pitch, select_kernel, empty_planes, conv2d_lowbit, conv_out_dim, gemm_grouped, gemm_lowbit_i8,
+    conv_select, CONV_PATH_ENCODE_GEMM, CONV_PATH_IMPLICIT_I8, CONV_PATH_IMPLICIT_FP4, CONV_PATH_HALO_FP4,
 )

@@ -111,6 +111,9 @@ SIGNATURES = {
     "lowbit_debug_pair_stats": (_I, [C.POINTER(C.c_ulonglong)]),
     "lowbit_debug_fp4_stats": (_I, [C.POINTER(C.c_ulonglong)]),
     "lowbit_debug_conv_trace": (_I, [C.POINTER(C.c_ulonglong)]),
+    "lowbit_debug_halo_trace": (_I, [C.POINTER(C.c_ulonglong)]),
+    "lowbit_debug_halo_phases": (_I, [C.POINTER(C.c_ulonglong), _I]),
+    "lowbit_conv_select": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I]),
     "lowbit_gemm_i8": (_I, [_I, _P, _LL, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _LL, _P]),
     "lowbit_select_kernel": (_I, [_I, _I, _I, _I]),
     "lowbit_gemm_lowbit_host": (_I, [_I, _P, _P, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P]),

@@ -182,6 +182,16 @@ def select_kernel(mode: int, m: int, n: int, k: int) -> int:
     return int(L.lib.lowbit_select_kernel(mode, m, n, k))
 
 
+CONV_PATH_ENCODE_GEMM, CONV_PATH_IMPLICIT_I8, CONV_PATH_IMPLICIT_FP4, CONV_PATH_HALO_FP4 = 1, 3, 6, 7
+
+
+def conv_select(mode: int, fm_binary: bool, batch: int, h: int, w: int, c: int, cout: int, kh: int, kw: int,
+                stride: int = 1, padding: int = 0, kernel: int = KERNEL_AUTO, has_workspace: bool = True) -> int:
+    """The kernel conv2d_lowbit takes for this conv (lowbit_conv_select; host logic, no GPU needed)."""
+    return int(L.lib.lowbit_conv_select(mode, int(fm_binary), batch, h, w, c, cout, kh, kw, stride, padding, kernel,
+                                        int(has_workspace)))
+
+
 def conv_out_dim(i: int, k: int, s: int, p: int) -> int:
     """conv.cpp:5-7"""
     return (i + 2 * p - k) // s + 1

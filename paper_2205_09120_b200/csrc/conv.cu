@@ -161,6 +161,32 @@ extern "C" size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int 
     return planes > fm4 ? planes : fm4;
 }
 
+// Which conv kernel lowbit_conv2d runs (pointers assumed aligned; host logic only):
+//   K7 fused halo conv — stride 1, the padded row fits 128 pixels, c % 128 == 0, padding that
+//      reads as 0 (ternary map or no padding), the filter + two halo stages fit in shared memory;
+//   K6 fp4 implicit GeMM over a packed fp4 copy of the map — same padding rule, any stride (needs
+//      the workspace);
+//   int8 implicit GeMM (TMA im2col over the int8 map) — TNN/TBN, c % 128 == 0, padding reads 0;
+//   else K4 (fused im2col + encode) + lowbit_gemm.
+// BNN maps padded with +-1 always take the last path: TMA's out-of-bounds fill is 0 and a 0
+// activation must raise ZeroInBinaryInput (conv.cpp:13, core.cpp:23).
+extern "C" int lowbit_conv_select(int mode, int fm_binary, int batch, int h, int w, int c, int cout, int kh, int kw,
+                                  int stride, int padding, int kernel, int has_workspace) {
+    const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
+    const bool tensor = kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR;
+    static const bool no_halo = getenv("LOWBIT_CONV_NO_HALO") != nullptr;  // tuning experiment knob
+    if (rows <= 0) return LOWBIT_CONV_PATH_ENCODE_GEMM;
+    if (tensor && !no_halo && lb::conv_halo_applies(fm_binary, h, w, c, cout, kh, kw, stride, padding, batch))
+        return LOWBIT_CONV_PATH_HALO_FP4;
+    if (tensor && has_workspace && lb::conv_fp4_applies(mode, fm_binary, c, cout, kh, kw, padding, rows, stride))
+        return LOWBIT_CONV_PATH_IMPLICIT_FP4;
+    const bool pad_is_zero = padding == 0 || !fm_binary;
+    if (mode != LOWBIT_BNN && pad_is_zero && c % 128 == 0 && rows <= 0x7FFFFFFFLL &&
+        (tensor || kernel == LOWBIT_KERNEL_TENSOR_I8))
+        return LOWBIT_CONV_PATH_IMPLICIT_I8;
+    return LOWBIT_CONV_PATH_ENCODE_GEMM;
+}
+
 extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
                                        const void* weights, int b_ternary, int cout, int k, int kh, int kw, int stride,
                                        int padding, int binary_pad_value, void* workspace, int* zero_flag,
@@ -174,25 +200,19 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
     // activations, or no padding — and the channel count tiles into 128-byte
     // k-blocks.  BNN keeps the bit path: its padding is +-1 and a 0 activation
     // must raise ZeroInBinaryInput (conv.cpp:13, core.cpp:23).
-    const bool pad_is_zero = padding == 0 || !fm_binary;
-    // K7, fused halo convolution on the fp4 tensor cores (stride 1, no workspace)
-    static const bool no_halo = getenv("LOWBIT_CONV_NO_HALO") != nullptr;  // tuning experiment knob
-    if ((kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) && !no_halo &&
-        lb::conv_halo_applies(fm_binary, h, w, c, cout, kh, kw, stride, padding, batch) &&
-        (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
-        (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+    const bool aligned = (reinterpret_cast<uintptr_t>(fm) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
+                         (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    const int path = aligned ? lowbit_conv_select(mode, fm_binary, batch, h, w, c, cout, kh, kw, stride, padding,
+                                                  kernel, workspace != nullptr)
+                             : LOWBIT_CONV_PATH_ENCODE_GEMM;
+    if (path == LOWBIT_CONV_PATH_HALO_FP4)
         return lb::launch_conv_halo(fm, batch, h, w, c, kh, kw, padding, mode == LOWBIT_BNN && fm_binary, weights,
                                     b_ternary, cout, out, zero_flag, (cudaStream_t)stream);
-    // K6, fp4 implicit GeMM over a packed fp4 copy of the feature map (workspace)
-    if ((kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR) && workspace &&
-        lb::conv_fp4_applies(mode, fm_binary, c, cout, kh, kw, padding, rows, stride) &&
-        (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
-        (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+    if (path == LOWBIT_CONV_PATH_IMPLICIT_FP4)
         return lb::launch_conv_fp4(fm, batch, h, w, c, kh, kw, stride, padding, mode == LOWBIT_BNN && fm_binary,
                                    weights, b_ternary, cout, out, workspace, zero_flag, (cudaStream_t)stream);
-    if (mode != LOWBIT_BNN && pad_is_zero && c % 128 == 0 && rows <= 0x7FFFFFFFLL &&
-        (kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR || kernel == LOWBIT_KERNEL_TENSOR_I8) &&
-        (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 255) == 0)
+    if (path == LOWBIT_CONV_PATH_IMPLICIT_I8)
         return lb::launch_conv_pair_im2col(fm, batch, h, w, c, kh, kw, stride, padding, weights, b_ternary, cout, out,
                                            (cudaStream_t)stream);
     if (!workspace) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d: NULL workspace");

@@ -83,3 +83,31 @@ def test_select_kernel_table():
     # launch-bound shapes take the int8 tensor kernel (c1, the c2 sweep)
     assert L.lib.lowbit_select_kernel(L.TBN, 72, 24, 128) == L.KERNEL_TENSOR_I8
     assert L.lib.lowbit_select_kernel(L.TNN, 360, 96, 256) == L.KERNEL_TENSOR_I8
+
+
+def test_conv_select_paths():
+    """lowbit_conv_select: which conv kernel conv2d_lowbit takes (conv.cu)."""
+    sel = lb.conv_select
+    # config 4: 64 x 56 x 56 x 128, 3x3 -> 128, stride 1, pad 1, ternary map -> K7 fused halo
+    assert sel(L.TNN, False, 64, 56, 56, 128, 128, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
+    assert sel(L.TBN, False, 64, 56, 56, 128, 128, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
+    # several n tiles (cout 496 -> 3 x 176), two channel blocks, 128-pixel rows, a 5x5 filter
+    assert sel(L.TNN, False, 2, 14, 14, 128, 496, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
+    assert sel(L.TNN, False, 2, 9, 9, 256, 64, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
+    assert sel(L.TNN, False, 1, 3, 100, 128, 96, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
+    assert sel(L.TBN, False, 2, 11, 13, 128, 64, 5, 5, 1, 2) == lb.CONV_PATH_HALO_FP4
+    # a filter too large for K7 / K6's shared memory: the int8 implicit GeMM
+    assert sel(L.TNN, False, 3, 10, 9, 256, 400, 3, 3, 1, 1) == lb.CONV_PATH_IMPLICIT_I8
+    # binary map without padding: K7 (the converters raise ZeroInBinaryInput)
+    assert sel(L.BNN, True, 2, 7, 7, 128, 64, 3, 3, 1, 0) == lb.CONV_PATH_HALO_FP4
+    # stride 2: the fp4 implicit GeMM with a workspace, else the int8 one
+    assert sel(L.TNN, False, 3, 8, 7, 128, 96, 3, 3, 2, 1) == lb.CONV_PATH_IMPLICIT_FP4
+    assert sel(L.TNN, False, 3, 8, 7, 128, 96, 3, 3, 2, 1, has_workspace=False) == lb.CONV_PATH_IMPLICIT_I8
+    # padded row wider than 128 pixels: K6
+    assert sel(L.TNN, False, 1, 2, 130, 128, 24, 3, 3, 1, 1) == lb.CONV_PATH_IMPLICIT_FP4
+    # BNN map padded with +-1, or c not a multiple of 128: K4 encode + GeMM
+    assert sel(L.BNN, True, 64, 56, 56, 128, 128, 3, 3, 1, 1) == lb.CONV_PATH_ENCODE_GEMM
+    assert sel(L.TNN, False, 1, 9, 9, 64, 32, 3, 3, 1, 1) == lb.CONV_PATH_ENCODE_GEMM
+    # the int8 kernel request skips the fp4 ones; the bit-serial request takes the bit path
+    assert sel(L.TNN, False, 64, 56, 56, 128, 128, 3, 3, 1, 1, kernel=L.KERNEL_TENSOR_I8) == lb.CONV_PATH_IMPLICIT_I8
+    assert sel(L.TNN, False, 64, 56, 56, 128, 128, 3, 3, 1, 1, kernel=L.KERNEL_BITSERIAL) == lb.CONV_PATH_ENCODE_GEMM

@@ -164,3 +164,31 @@ def test_gemm_from_int8(lb, port, mode):
         bp = lb.encode_ternary(torch.from_numpy(b).cuda()) if mode == TNN else lb.encode_binary(torch.from_numpy(b).cuda())
         got = lb.gemm_lowbit_i8(mode, torch.from_numpy(a).cuda(), lb.prepare_weights(lb.pack_b(bp)), (m, n, k))
         assert (got.cpu().numpy() == port.gemm(mode, a, b)).all(), (mode, m, n, k)
+
+
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_conv_halo_geometries(lb, port, mode):
+    """K7 (fused halo conv) across its geometry: position pitch 32 / 64 / 128
+    (4, 2 or 1 output rows per CTA tile, output heights not a multiple of
+    them), two channel blocks, several n tiles, 1x1 / 3x3 / 5x5 filters, an
+    odd number of CTA tiles (the idle CTA of the last pair), padding 0 / 1 /
+    2 — each checked to run on K7 (lowbit_conv_select), then against the
+    oracle's direct convolution (test_conv.cpp:22-47)."""
+    da, db = mode_dists(mode)
+    cases = [(2, 7, 14, 128, 64, 3, 1), (1, 3, 100, 128, 96, 3, 1), (2, 9, 9, 256, 64, 3, 1),
+             (2, 14, 14, 128, 496, 3, 1), (3, 11, 13, 128, 64, 5, 2), (1, 5, 40, 128, 32, 1, 0),
+             (1, 1, 1, 128, 8, 3, 1)]
+    for i, (b, h, w, ch, cout, ksz, pad) in enumerate(cases):
+        if mode == BNN:
+            pad = 0  # a binary map pads with +-1: K4's path (test_conv_binary_pad_values)
+            if h < ksz or w < ksz:
+                continue
+        assert lb.conv_select(mode, mode == BNN, b, h, w, ch, cout, ksz, ksz, 1, pad) == lb.CONV_PATH_HALO_FP4, \
+            (b, h, w, ch, cout, ksz, pad)
+        fm = port.generate(da, 150 + i, 0, b * h * w, ch).reshape(b, h, w, ch)
+        wt = port.generate(db, 150 + i, 1, ksz * ksz * ch, cout)
+        got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), mode == BNN, weights_for(lb, wt, mode), ksz, ksz, 1,
+                               pad).cpu().numpy()
+        for img in range(b):
+            want = port.direct_conv(fm[img], mode == BNN, wt, ksz, ksz, 1, pad)
+            assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, ch, cout, ksz, pad, img)
