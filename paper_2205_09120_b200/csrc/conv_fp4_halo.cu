@@ -131,6 +131,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H7_THREADS, 1)
                          const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
                          const HaloParams prm) {
     if (prm.dbg & 32768) return;  // launch-overhead probe
+    // programmatic dependent launch: this grid may be launched while the previous kernel
+    // in the stream drains; nothing below reads global memory before that kernel is done
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if ((prm.dbg & 32) && threadIdx.x == 0) atomicMin(&g_halo_phase[0], h7_gtime());
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -589,7 +592,18 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
         attr = true;
     }
     const int pairs = prm.ptiles < num_sms() / 2 ? prm.ptiles : num_sms() / 2;
-    conv_fp4_halo_kernel<<<2 * pairs, H7_THREADS, H7_SMEM, stream>>>(mb, mraw, mc64, mc16, prm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(H7_THREADS);
+    cfg.dynamicSmemBytes = H7_SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    static const bool no_pdl = getenv("LOWBIT_NO_PDL") != nullptr;  // tuning experiment knob
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LB_CUDA_TRY(cudaLaunchKernelEx(&cfg, conv_fp4_halo_kernel, mb, mraw, mc64, mc16, prm));
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }
