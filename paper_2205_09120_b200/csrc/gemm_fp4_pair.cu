@@ -115,7 +115,8 @@ struct Fp4Params {
     int a_res;     // AR variant (launch selects the template; recorded for the host only)
     int debug;  // LOWBIT_DEBUG_FP4 timing experiments (results invalid unless only 8 is set): 1 converters
                 // skip the expansion, 2 no MMAs, 4 no epilogue, 8 role timers (valid), 16 MMA issue without
-                // waits, 64 half the B loads, 128 no TMA stores, 256 no TMEM loads, 512 no staging stores
+                // waits, 64 half the B loads, 128 no TMA stores, 256 no TMEM loads, 512 no staging stores,
+                // 4096 C stores evict_first, 8192 B loads without the evict_last hint
 };
 
 // Role timing for profiling experiments (LOWBIT_DEBUG_FP4 bit 3): cycle
@@ -278,6 +279,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     mbar_wait_sleep(&raw_empty[rs], ((u / RS) & 1) ^ 1);
                     uint8_t* raw = sRaw + rs * RAW_SLOT;
                     mbar_arrive_expect_tx(&raw_full[rs], RAW_SLOT);
+                    // (marking these streamed planes evict_first measured 10% slower on config 5)
                     tma_load_2d(raw, &tmap_a0, &raw_full[rs], kb * 32, arow);
                     if (A_TER) tma_load_2d(raw + F4_RAW_PLANE, &tmap_a1, &raw_full[rs], kb * 32, arow);
                 }
@@ -288,6 +290,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
         if (lane == 0) {
             const uint32_t pair_bytes = (uint32_t)bn * 128;
             const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), pbase);
+            // B (the weights) is re-read by every pair for every m tile while A and C stream
+            // through L2 once: keep it resident (evict_last; +3% on config 5)
+            const uint64_t b_policy = l2_policy_evict_last();
             uint32_t t = 0;
             for (int i = 0; AR && i < my_tiles; ++i) {
                 // AR: stages of two k-blocks (one barrier per 8 MMAs: an mbarrier wait on
@@ -305,9 +310,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                                             (uint16_t)((1u << rank) | (1u << (rank + 2))));
                         continue;
                     }
-                    for (int j = 0; j < 2; ++j)
-                        tma_load_2d_pair(smem_u32(sB + (2 * st + j) * B_BYTES), &tmap_b, b_full0 + st * 8,
-                                         (kb + j) * 128, brow);
+                    for (int j = 0; j < 2; ++j) {
+                        if (!(prm.debug & 8192))
+                            tma_load_2d_pair_hint(smem_u32(sB + (2 * st + j) * B_BYTES), &tmap_b, b_full0 + st * 8,
+                                                  (kb + j) * 128, brow, b_policy);
+                        else
+                            tma_load_2d_pair(smem_u32(sB + (2 * st + j) * B_BYTES), &tmap_b, b_full0 + st * 8,
+                                             (kb + j) * 128, brow);
+                    }
                 }
             }
             for (int i = 0; g2 && i < my_tiles; ++i) {
@@ -319,8 +329,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     mbar_wait_sleep(&a_empty[st], ((t >> 2) & 1) ^ 1);
                     if (leader) mbar_arrive_expect_tx(&b_full[st], 2 * pair_bytes);
                     for (int j = 0; j < 2; ++j)
-                        tma_load_2d_pair(smem_u32(sB + (2 * st + j) * F4_B_BYTES), &tmap_b, b_full0 + st * 8,
-                                         (kb + j) * 128, brow);
+                        tma_load_2d_pair_hint(smem_u32(sB + (2 * st + j) * F4_B_BYTES), &tmap_b, b_full0 + st * 8,
+                                              (kb + j) * 128, brow, b_policy);
                 }
             }
             for (int i = 0; !AR && !g2 && i < my_tiles; ++i) {
@@ -335,7 +345,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         continue;
                     }
                     if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
-                    tma_load_2d_pair(smem_u32(sB + st * F4_B_BYTES), &tmap_b, b_full0 + st * 8, kb * 128, brow);
+                    tma_load_2d_pair_hint(smem_u32(sB + st * F4_B_BYTES), &tmap_b, b_full0 + st * 8, kb * 128, brow,
+                                          b_policy);
                 }
             }
         }
@@ -698,8 +709,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int j = 0; j < EGRP && g0 + j < cend; ++j)
-                            tma_store_2d(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16, row0);
+                        for (int j = 0; j < EGRP && g0 + j < cend; ++j) {
+                            if (prm.debug & 4096)
+                                tma_store_2d_hint(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16,
+                                                  row0, l2_policy_evict_first());
+                            else
+                                tma_store_2d(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16, row0);
+                        }
                         bulk_commit();
                     }
                 }

@@ -161,6 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             // both CTAs' halves of B (+ both CTAs' int8 A tiles when A comes straight from TMA)
             const uint32_t pair_bytes = (uint32_t)bn * PR_BK + (LAYOUT >= 2 ? 2 * PR_A_BYTES : 0);
             const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
+            const uint64_t b_policy = l2_policy_evict_last();
             uint32_t t = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
@@ -177,7 +178,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     const uint32_t st = t % PR_B_STAGES;
                     mbar_wait_sleep(&a_empty[st], ((t / PR_B_STAGES) & 1) ^ 1);  // shared ring: A/B slot free
                     if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
-                    tma_load_2d_pair(smem_u32(sB + st * PR_B_BYTES), &tmap_b, b_full0 + st * 8, kb * PR_BK, brow);
+                    // the weights are re-read for every m tile: keep them in L2 (evict_last)
+                    tma_load_2d_pair_hint(smem_u32(sB + st * PR_B_BYTES), &tmap_b, b_full0 + st * 8, kb * PR_BK, brow,
+                                          b_policy);
                     if (LAYOUT == 2) {  // dense int8 A: 128 rows x 128 depth, 128B swizzle = the UMMA tile
                         tma_load_2d_pair(smem_u32(sA + st * PR_A_BYTES), &tmap_a0, b_full0 + st * 8, kb * PR_BK, arow);
                     } else if (LAYOUT == 3) {  // implicit GeMM: tap (ky, kx), 128 channels, 128 output pixels

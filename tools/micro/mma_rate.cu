@@ -437,7 +437,95 @@ void k5_pipe_run(int stages) {
     cudaFree(d);
 }
 
+// K5's streaming issue loop verbatim in shape: per k-block a tcgen05 fence,
+// lane 0 issues 4 N = 256 MMAs over a 4-stage ring of A / B slots (SW128)
+// and VARIANT commits, then the warp re-converges.
+//   VARIANT 0: one commit (local)       1: two commits multicast to both CTAs
+//   2: two multicast commits, whole-warp loop (no lane-0 branch for the MMAs)
+template <int VARIANT>
+__global__ void __launch_bounds__(128, 1) k5_loop_kernel(int kblocks, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    for (int i = threadIdx.x; i < 4 * 32768 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x22A022A0u ^ (i * 0x01010101u & 0x08080808u);
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __shared__ uint32_t tslot;
+    __shared__ uint64_t e1[4], e2[4], done;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) { for (int q = 0; q < 4; ++q) { mbar_init(&e1[q], 1); mbar_init(&e2[q], 1); } mbar_init(&done, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc_pair<512>(&tslot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tb = tslot;
+    {
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        tmem_st_32x32b_x8_fill(tb + lane_base + 256 + 248, 0x7F7F7F7Fu);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (cluster_ctarank() == 0 && warp == 0) {
+        const uint32_t base = smem_u32(smem);
+        const uint32_t id = idesc_mxf4(256, 256);
+        const long long t0 = clock64();
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const uint32_t sa = kb & 3;
+            tc_fence_after();
+            if (VARIANT == 2 || lane == 0) {
+                const uint32_t a_addr = base + sa * 16384, b_addr = base + 65536 + sa * 16384;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_mxf4_pair(tb, umma_desc_k_sw128(a_addr + kk * 32), umma_desc_k_sw128(b_addr + kk * 32), id,
+                                   tb + 504, tb + 504, (kb | kk) != 0);
+                if (VARIANT == 0) {
+                    umma_commit_pair(&e1[sa], 0x1);
+                } else {
+                    umma_commit_pair(&e1[sa], 0x3);
+                    umma_commit_pair(&e2[sa], 0x3);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            umma_commit_pair(&done, 0x1);
+            mbar_wait(&done, 0);
+            out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc_pair<512>(tb); }
+}
+
+template <int VARIANT>
+void k5_loop_run(int kblocks) {
+    auto k = k5_loop_kernel<VARIANT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    unsigned long long* d; cudaMalloc(&d, 148 * 8); cudaMemset(d, 0, 148 * 8);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = 148; cfg.blockDim = 128; cfg.dynamicSmemBytes = 131072;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, kblocks, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[148]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    unsigned long long mx = 0;
+    for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("K5 loop variant %d (%s): %s %.1f cycles per MMA\n", VARIANT,
+           VARIANT == 0 ? "1 local commit per k-block" : VARIANT == 1 ? "2 multicast commits per k-block" : "2 multicast commits, whole warp issues",
+           cudaGetErrorString(err), (double)mx / kblocks / 4);
+    cudaFree(d);
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == 'l') {
+        k5_loop_run<0>(50000); k5_loop_run<1>(50000);
+        return 0;
+    }
     if (argc > 1 && argv[1][0] == 'k') {
         k5_pipe_run<1>(4000); k5_pipe_run<2>(4000);
         return 0;
