@@ -94,6 +94,7 @@ constexpr int F4_AR_RAW = LOWBIT_F4_AR_RAW_KB * 1024;
 constexpr int F4_AR_BN = LOWBIT_F4_AR_BN, F4_AR_B_SLOTS = LOWBIT_F4_AR_B_SLOTS, F4_AR_EGRP = LOWBIT_F4_AR_EGRP;
 constexpr int F4_AR_B_BYTES = (F4_AR_BN / 2) * 128;
 static_assert(F4_AR_B_BYTES % 1024 == 0 && F4_AR_B_SLOTS % 2 == 0, "AR B slots");
+static_assert(F4_AR_EGRP == 2, "the epilogue stores 32-column boxes: groups of two 16-column chunks");
 // staging: 8 epilogue warps x F4_AR_EGRP (AR) or 4 warps x 2 buffers of 1 KB
 __host__ __device__ constexpr int f4_epi_bytes(bool ar) { return (ar ? 8 * F4_AR_EGRP : 8) * F4_EPI_BYTES; }
 __host__ __device__ constexpr int f4_smem_bytes(bool ar) {
@@ -116,7 +117,7 @@ struct Fp4Params {
     int debug;  // LOWBIT_DEBUG_FP4 timing experiments (results invalid unless only 8 is set): 1 converters
                 // skip the expansion, 2 no MMAs, 4 no epilogue, 8 role timers (valid), 16 MMA issue without
                 // waits, 64 half the B loads, 128 no TMA stores, 256 no TMEM loads, 512 no staging stores,
-                // 4096 C stores evict_first, 8192 B loads without the evict_last hint
+                // 8192 B loads without the evict_last hint
 };
 
 // Role timing for profiling experiments (LOWBIT_DEBUG_FP4 bit 3): cycle
@@ -596,7 +597,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
         const int wq = warp & 3;            // TMEM lane quarter (warp % 4, as tcgen05.ld/st require)
         const int half = ewarp >> 2;        // column range of the tile this warp drains
         constexpr int NHALF = EPI_W / 4;
-        const int nch_all = bn / 16, per_half = (nch_all + NHALF - 1) / NHALF;
+        // chunk ranges of an even length (bn is a multiple of 32): whole 32-column store boxes
+        const int nch_all = bn / 16, per_half = ((nch_all + NHALF - 1) / NHALF + 1) & ~1;
         const int ch_lo = half * per_half, ch_hi = ch_lo + per_half < nch_all ? ch_lo + per_half : nch_all;
         // the warps draining the last chunk also own the scale hand-off (sf_ready counts 8)
         const bool sf_owner = half == (nch_all - 1) / per_half;
@@ -686,10 +688,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         if (prm.debug & 512) {  // timing experiment: no staging stores
                             if ((h[0] ^ h[3] ^ h[7]) == 0x9E3779B9u && lane == 77) sts_v4(epi, h[0], h[1], h[2], h[3]);
                         } else if (prm.tma_store) {
-                            const uint32_t rowaddr = epi + (uint32_t)j * F4_EPI_BYTES + lane * 32;
-                            const uint32_t sw = (uint32_t)(lane >> 2) & 1;  // TMA SWIZZLE_32B
-                            sts_v4(rowaddr + (sw << 4), h[0], h[1], h[2], h[3]);
-                            sts_v4(rowaddr + ((sw ^ 1) << 4), h[4], h[5], h[6], h[7]);
+                            // chunk j of the group's 32-column box: 64-byte rows, TMA SWIZZLE_64B
+                            const uint32_t rowaddr = epi + lane * 64;
+                            const uint32_t swz = ((uint32_t)lane >> 1) & 3;
+                            sts_v4(rowaddr + (((2u * j) ^ swz) << 4), h[0], h[1], h[2], h[3]);
+                            sts_v4(rowaddr + (((2u * j + 1) ^ swz) << 4), h[4], h[5], h[6], h[7]);
                         } else {
                             const int row = row0 + lane;
                             if (row < prm.m) {
@@ -709,13 +712,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int j = 0; j < EGRP && g0 + j < cend; ++j) {
-                            if (prm.debug & 4096)
-                                tma_store_2d_hint(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16,
-                                                  row0, l2_policy_evict_first());
-                            else
-                                tma_store_2d(&tmap_c, epi + (uint32_t)j * F4_EPI_BYTES, nt * bn + (g0 + j) * 16, row0);
-                        }
+                        // one 32-column box per group: half the TMA store rows of 16-column boxes
+                        // (the store rows share the TMA unit with the B loads): +3.5% on c3 / c5
+                        tma_store_2d(&tmap_c, epi, nt * bn + g0 * 16, row0);
                         bulk_commit();
                     }
                 }
@@ -762,11 +761,12 @@ extern "C" int lowbit_debug_fp4_stats(unsigned long long* out16) {
 namespace lb {
 
 // BN: the fewest column tiles of <= 256 (an MMA costs the same for any N <= 256),
-// then the smallest multiple of 16 covering n (less B traffic).
+// then the smallest multiple of 32 covering n: the epilogue stores 32-column boxes
+// (two 16-column chunks), so every warp's chunk range is a whole number of pairs.
 static int pick_bn_fp4(int n, int max_bn = F4_MAX_BN) {
     const int tiles = (n + max_bn - 1) / max_bn;
     const int per = (n + tiles - 1) / tiles;
-    return (per + 15) / 16 * 16;
+    return (per + 31) / 32 * 32;
 }
 
 template <bool A_TER, bool AR, int LAYOUT, int CL = 2>
@@ -849,7 +849,7 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
                      CU_TENSOR_MAP_SWIZZLE_128B))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for fp4 B");
     if (prm.tma_store) {
-        if (!make_map_2d(&mc, c, (uint64_t)n, (uint64_t)m, (uint64_t)ldc * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B,
+        if (!make_map_2d(&mc, c, (uint64_t)n, (uint64_t)m, (uint64_t)ldc * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B,
                          CU_TENSOR_MAP_DATA_TYPE_UINT16))
             return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for C");
     } else {
