@@ -509,7 +509,8 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
     if (g.kblocks > H7_MAX_KB || cb * g.raw_cb > H7_RAW_MAX) return g;
     const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - H7_EPI_BYTES - g.kblocks * g.breg;
     // ring depths: fp4 3 (2 if tight), raw whatever is left (<= 4, >= 2)
-    for (int f4 = 3; f4 >= 2; --f4) {
+    static const int f4_max = getenv("LOWBIT_HALO_F4ST") ? atoi(getenv("LOWBIT_HALO_F4ST")) : 3;  // tuning knob
+    for (int f4 = f4_max; f4 >= 2; --f4) {
         const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
         if (raw >= 2) {
             g.f4_st = f4;
