@@ -551,7 +551,8 @@ def side_configs(lb, torch, flush, pk):
     # (name, A plane layout, kernel id, peak): K5 fp4 from the reference encoding (what AUTO runs) and
     # from nibble-interleaved planes, K3 int8 from lane-interleaved planes, K2 bit-serial
     variants = (("tensor_fp4", 0, lb.KERNEL_TENSOR, "fp4"), ("tensor_fp4_nibbles", 2, lb.KERNEL_TENSOR, "fp4"),
-                ("tensor_i8_lanes", 1, lb.KERNEL_TENSOR, "i8"), ("bitserial", 0, lb.KERNEL_BITSERIAL, "popc"))
+                ("tensor_i8_lanes", 1, lb.KERNEL_TENSOR, "i8"), ("bitserial", 0, lb.KERNEL_BITSERIAL, "popc"),
+                ("auto_reference_planes", 0, lb.KERNEL_AUTO, "auto"))
     for name in ("c1", "c3"):
         mode, M, N, K, da, db, seed = CONFIGS[name]
         a = lb.generate(da, seed, 0, M, K)
@@ -565,10 +566,13 @@ def side_configs(lb, torch, flush, pk):
             f = lambda: lb.gemm_lowbit(mode, planes[lay], w, (M, N, K), kernel=kid, out=c)
             ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
             tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
+            if pkind == "auto":  # the kernel lowbit_select_kernel picks for this shape
+                pkind = "fp4" if lb.select_kernel(mode, M, N, K) == lb.KERNEL_TENSOR else "i8"
             peak = {"fp4": fp4_peak, "i8": tensor_peak}.get(pkind) or popc(mode)
             res[kn] = {"ms": ms, "TOPS": tops, "frac": tops / peak,
                        "bound": "popc" if kn == "bitserial" else "tensor"}
-        res["auto"] = {2: "tensor_fp4", 4: "tensor_i8 (reference planes)"}.get(lb.select_kernel(mode, M, N, K))
+        res["auto"] = {2: "tensor_fp4", 3: "tensor_1cta (int8, single-CTA; reference planes)",
+                       4: "tensor_i8 (reference planes)"}.get(lb.select_kernel(mode, M, N, K))
         res["timing"] = "cuda graph replay" if name == "c1" else "events, L2 flushed"
         out[name] = res
     # c2: the 64-shape TBN sweep (one launch per shape), captured as one graph

@@ -130,7 +130,11 @@ static lowbit_status validate_gemm(int mode, bool a_ternary, int b_ternary, int 
 extern "C" int lowbit_select_kernel(int mode, int m, int n, int k) {
     (void)mode;
     const double ops = 2.0 * (double)m * (double)n * (double)k;
-    return ops < 1e9 ? LOWBIT_KERNEL_TENSOR_I8 : LOWBIT_KERNEL_TENSOR;
+    // launch-bound shapes (< ~1 GOP): the int8 kernel; up to 4 row tiles the single-CTA
+    // variant (its smaller launch: config 1 4.4 vs 5.2 us per call; the config-2 sweep is
+    // a tie, tools/c1_latency.py); above that the fp4 kernel
+    if (ops < 1e9) return m <= 512 ? LOWBIT_KERNEL_TENSOR_1CTA : LOWBIT_KERNEL_TENSOR_I8;
+    return LOWBIT_KERNEL_TENSOR;
 }
 
 extern "C" lowbit_status lowbit_gemm(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int a_rows,
