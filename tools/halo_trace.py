@@ -42,3 +42,5 @@ print("steady state (tiles 4-11): producer period %.0f, raw latency issue->conve
           avg([ev[0][i + 1] - ev[0][i] for i in T]), avg([ev[1][i] - ev[0][i] for i in T]),
           avg([ev[3][i] - ev[2][i] for i in T]), avg([ev[6][i] - ev[5][i] for i in T]),
           avg([ev[6][i + 1] - ev[6][i] for i in T]), avg([ev[9][i] - ev[7][i] for i in T])))
+print("MMA waits per tile (tiles 4-11): tmem_empty->a_full %.0f, a_full->issued %.0f; converter done -> MMA a_full %.0f" % (
+    avg([ev[5][i] - ev[4][i] for i in T]), avg([ev[6][i] - ev[5][i] for i in T]), avg([ev[5][i] - ev[3][i] for i in T])))

@@ -281,16 +281,22 @@ void conv_run(int n, int iters) {
 // (the first with accumulate = 0) on a ring of NACC accumulators, one commit
 // per tile, NISS issuing warps on alternate tiles, each waiting for the
 // commit of the tile NACC back before reusing its accumulator.
-template <int NISS, int NACC>
+template <int NISS, int NACC, int XWAIT = 0, int XCOMMIT = 0>
 __global__ void __launch_bounds__(128, 1) conv_pipe_kernel(int tiles, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     for (int i = threadIdx.x; i < 4 * 32768 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x22A022A0u ^ (i * 0x01010101u & 0x08080808u);
     __syncthreads();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __shared__ uint32_t tslot;
-    __shared__ uint64_t full[4];
+    __shared__ uint64_t full[4], xbar, xc[4];
     const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) { for (int a = 0; a < 4; ++a) mbar_init(&full[a], 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 4; ++a) { mbar_init(&full[a], 1); mbar_init(&xc[a], 1); }
+        mbar_init(&xbar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive(&xbar);
     if (warp == 0) tmem_alloc_pair<512>(&tslot);
     tc_fence_before();
     cluster_sync();
@@ -315,6 +321,7 @@ __global__ void __launch_bounds__(128, 1) conv_pipe_kernel(int tiles, unsigned l
         for (int t = warp; t < tiles; t += NISS) {
             const int acc = t % NACC;
             if (t >= NACC) mbar_wait(&full[acc], ((t / NACC) - 1) & 1);
+            if (XWAIT) mbar_wait_poll(&xbar, 0);  // a second (already complete) barrier per tile, as K7's a_full
             tc_fence_after();
             const uint32_t d = tb + (uint32_t)acc * 160u;
 #pragma unroll
@@ -323,6 +330,7 @@ __global__ void __launch_bounds__(128, 1) conv_pipe_kernel(int tiles, unsigned l
                 umma_mxf4_pair(d, ad, bd, id, tb + 480, tb + 480, kb != 0);
                 umma_mxf4_pair(d, ad + 2, bd + 2, id, tb + 480, tb + 480, 1);
             }
+            if (XCOMMIT) umma_commit_pair(&xc[acc], 0x3);  // K7 also commits the A stage to both CTAs
             umma_commit_pair(&full[acc], 0x1);
         }
         // drain: wait for this issuer's last tile
@@ -336,9 +344,9 @@ __global__ void __launch_bounds__(128, 1) conv_pipe_kernel(int tiles, unsigned l
     if (warp == 0) { tc_fence_after(); tmem_dealloc_pair<512>(tb); }
 }
 
-template <int NISS, int NACC>
+template <int NISS, int NACC, int XWAIT = 0, int XCOMMIT = 0>
 void pipe_run(int tiles) {
-    auto k = conv_pipe_kernel<NISS, NACC>;
+    auto k = conv_pipe_kernel<NISS, NACC, XWAIT, XCOMMIT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
     unsigned long long* d; cudaMalloc(&d, 148 * 16); cudaMemset(d, 0, 148 * 16);
     cudaLaunchConfig_t cfg = {};
@@ -352,8 +360,8 @@ void pipe_run(int tiles) {
     unsigned long long h[296]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
     unsigned long long mx = 0;
     for (int i = 0; i < 296; ++i) mx = h[i] > mx ? h[i] : mx;
-    printf("conv pipe: %d issuer(s), %d accumulators, %d tiles of 18 MMAs: %s %.1f cycles per tile (%.1f per MMA)\n", NISS, NACC,
-           tiles, cudaGetErrorString(err), (double)mx / tiles, (double)mx / tiles / 18);
+    printf("conv pipe: %d issuer(s), %d accumulators, extra wait %d, extra commit %d, %d tiles of 18 MMAs: %s %.1f cycles per tile (%.1f per MMA)\n", NISS, NACC,
+           XWAIT, XCOMMIT, tiles, cudaGetErrorString(err), (double)mx / tiles, (double)mx / tiles / 18);
     cudaFree(d);
 }
 
@@ -531,7 +539,7 @@ int main(int argc, char** argv) {
         return 0;
     }
     if (argc > 2) {
-        pipe_run<1, 3>(2000); pipe_run<2, 3>(2000); pipe_run<1, 2>(2000); pipe_run<2, 2>(2000);
+        pipe_run<2, 3>(2000); pipe_run<2, 3, 1>(2000); pipe_run<2, 3, 0, 1>(2000); pipe_run<2, 3, 1, 1>(2000);
         return 0;
     }
     if (argc > 1) {
