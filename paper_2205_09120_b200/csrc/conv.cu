@@ -80,6 +80,86 @@ __global__ void conv_encode_kernel(int a_binary, const int8_t* __restrict__ fm, 
     if (saw_zero && zero_flag) atomicOr(zero_flag, 1);
 }
 
+// c % 32 == 0: every 32-value word of a row is 32 channels of one tap.  A block
+// takes one output row (img, oy) at a time: its kh input rows (padding
+// resolved: out-of-image pixels hold pad_value) are staged in shared memory
+// once, then threads walk the row's (ox, word) pairs with an incremental index
+// and build each word from shared memory.  Input bytes cross L2 -> SM kh
+// times instead of kh*kw times (im2col), and no per-word divisions remain.
+__global__ void conv_encode_rows_kernel(int a_binary, const int8_t* __restrict__ fm, ConvGeom g, int pad_value,
+                                        uint8_t* __restrict__ plane0, uint8_t* __restrict__ plane1, long long pitch,
+                                        int* zero_flag) {
+    extern __shared__ __align__(16) uint8_t conv_smem[];
+    const int wpr = (int)(pitch / 4), kwords = g.k / 32;
+    uint32_t* tap_of_word = reinterpret_cast<uint32_t*>(conv_smem);  // (ky << 24) | (kx << 16) | c0 / 32
+    int8_t* rows_s = reinterpret_cast<int8_t*>(conv_smem + ((wpr * 4 + 15) & ~15));  // [kh][w][c]
+    for (int wd = threadIdx.x; wd < wpr; wd += blockDim.x) {
+        uint32_t e = 0xFFFFFFFFu;  // past the depth: a zero word
+        if (wd < kwords) {
+            const int k0 = wd * 32, tap = k0 / g.c, c0 = k0 - tap * g.c;
+            const int ky = tap / g.kw, kx = tap - ky * g.kw;
+            e = ((uint32_t)ky << 24) | ((uint32_t)kx << 16) | (uint32_t)(c0 / 32);
+        }
+        tap_of_word[wd] = e;
+    }
+    const int per_row = g.ow * wpr;
+    const int ox_first = threadIdx.x / wpr, wd_first = threadIdx.x - ox_first * wpr;
+    const int dox = blockDim.x / wpr, dwd = blockDim.x - dox * wpr;
+    const long long row_bytes = (long long)g.w * g.c;  // one input row
+    const int row16 = (int)(row_bytes / 16);
+    const uint32_t padw = pad_value > 0 ? 0x01010101u : (pad_value < 0 ? 0xFFFFFFFFu : 0u);
+    bool saw_zero = false;
+    for (long long orow = blockIdx.x; orow < (long long)g.batch * g.oh; orow += gridDim.x) {
+        const int img = (int)(orow / g.oh), oy = (int)(orow - (long long)img * g.oh);
+        __syncthreads();  // the previous row's words are built
+        for (int ky = 0; ky < g.kh; ++ky) {  // stage input row y = oy*s + ky - pad (or padding)
+            const int y = oy * g.stride + ky - g.pad;
+            uint4* dst = reinterpret_cast<uint4*>(rows_s + (long long)ky * row_bytes);
+            if (y >= 0 && y < g.h) {
+                const uint4* src = reinterpret_cast<const uint4*>(fm + ((long long)img * g.h + y) * row_bytes);
+                for (int i = threadIdx.x; i < row16; i += blockDim.x) dst[i] = __ldg(src + i);
+            } else {
+                for (int i = threadIdx.x; i < row16; i += blockDim.x) dst[i] = make_uint4(padw, padw, padw, padw);
+            }
+        }
+        __syncthreads();
+        const long long r0 = orow * g.ow;  // first output pixel (GeMM row) of this output row
+        int ox = ox_first, wd = wd_first;
+        for (int t = threadIdx.x; t < per_row; t += blockDim.x) {
+            const uint32_t e = tap_of_word[wd];
+            uint32_t plus = 0, minus = 0;
+            if (e != 0xFFFFFFFFu) {
+                const int ky = (int)(e >> 24), kx = (int)((e >> 16) & 0xFF), c0 = (int)(e & 0xFFFF) * 32;
+                const int x = ox * g.stride + kx - g.pad;
+                if (x >= 0 && x < g.w) {
+                    const uint4* q = reinterpret_cast<const uint4*>(rows_s + (long long)ky * row_bytes +
+                                                                    (long long)x * g.c + c0);
+                    encode_word32_regs(q[0], q[1], plus, minus);
+                } else if (pad_value > 0) {
+                    plus = 0xFFFFFFFFu;
+                } else if (pad_value < 0) {
+                    minus = 0xFFFFFFFFu;
+                }
+                if (a_binary && (plus | minus) != 0xFFFFFFFFu) saw_zero = true;
+            }
+            const long long r = r0 + ox;
+            if (a_binary) {
+                reinterpret_cast<uint32_t*>(plane0 + r * pitch)[wd] = minus;
+            } else {
+                reinterpret_cast<uint32_t*>(plane0 + r * pitch)[wd] = plus;
+                reinterpret_cast<uint32_t*>(plane1 + r * pitch)[wd] = minus;
+            }
+            ox += dox;
+            wd += dwd;
+            if (wd >= wpr) {
+                wd -= wpr;
+                ++ox;
+            }
+        }
+    }
+    if (saw_zero && zero_flag) atomicOr(zero_flag, 1);
+}
+
 __global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict__ out, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         out[i] = in[i];
@@ -147,8 +227,23 @@ extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int 
     if ((pitch & 3) || pitch < (g.k + 7) / 8)
         return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv_encode: bad pitch");
     const long long work = (long long)batch * g.oh * g.ow * (pitch / 4);
-    conv_encode_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(a_binary, fm, g, pad_value, plane0,
-                                                                               plane1, pitch, zero_flag);
+    const int wpr = (int)(pitch / 4);
+    const long long smem = ((wpr * 4LL + 15) & ~15LL) + (long long)kh * w * c;
+    if (c % 32 == 0 && kh < 256 && kw < 256 && smem <= 160 * 1024 && (reinterpret_cast<uintptr_t>(fm) & 15) == 0) {
+        static int attr_bytes = 0;
+        if (smem > 48 * 1024 && smem > attr_bytes) {
+            LB_CUDA_TRY(cudaFuncSetAttribute(conv_encode_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+            attr_bytes = (int)smem;
+        }
+        const long long orows = (long long)batch * g.oh;
+        const int blocks = (int)(orows < 148LL * 8 ? orows : 148LL * 8);
+        conv_encode_rows_kernel<<<blocks, 256, (size_t)smem, (cudaStream_t)stream>>>(a_binary, fm, g, pad_value,
+                                                                                     plane0, plane1, pitch, zero_flag);
+    } else {
+        conv_encode_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(a_binary, fm, g, pad_value, plane0,
+                                                                                   plane1, pitch, zero_flag);
+    }
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

@@ -15,17 +15,22 @@ namespace lb {
 
 // One thread -> one 32-bit word of every plane of one row (32 values).
 // LAYOUT 0: the reference LSB-first layout; 1: the lane-interleaved B200 layout.
+// The (row, word) of each iteration advance by a fixed step (no 64-bit
+// division per word: it cost ~20% of the kernel at c5's 67M words).
 template <int LAYOUT>
 __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, int rows, int cols, long long ld,
                               uint8_t* __restrict__ plane0, uint8_t* __restrict__ plane1, long long pitch,
                               int* zero_flag) {
-    const long long words_per_row = pitch / 4;
+    const int words_per_row = (int)(pitch / 4);
     const long long total = (long long)rows * words_per_row;
     bool saw_zero = false;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long r = idx / words_per_row;
-        const int w = (int)(idx - r * words_per_row);
+    const long long first = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long step = (long long)gridDim.x * blockDim.x;
+    long long r = first / words_per_row;
+    int w = (int)(first - r * words_per_row);
+    const long long dr = step / words_per_row;
+    const int dw = (int)(step - dr * words_per_row);
+    for (long long idx = first; idx < total; idx += step) {
         const int c0 = w * 32;
         uint32_t minus = 0, plus = 0;
         if (c0 < cols) {
@@ -47,6 +52,12 @@ __global__ void encode_kernel(int ternary, const int8_t* __restrict__ values, in
             reinterpret_cast<uint32_t*>(plane1 + r * pitch)[w] = minus;
         } else {
             d0[w] = minus;  // binary: -1 -> 1, +1 -> 0 (core.cpp:24)
+        }
+        r += dr;
+        w += dw;
+        if (w >= words_per_row) {
+            w -= words_per_row;
+            ++r;
         }
     }
     if (saw_zero && zero_flag) atomicOr(zero_flag, 1);

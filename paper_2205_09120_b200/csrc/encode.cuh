@@ -6,6 +6,19 @@ namespace lb {
 
 __device__ __forceinline__ uint32_t valid_mask32(int nvals) { return nvals >= 32 ? 0xFFFFFFFFu : ((1u << nvals) - 1u); }
 
+// 32 int8 values already in registers (two 16-byte vectors) -> plus / minus words.
+__device__ __forceinline__ void encode_word32_regs(const uint4 lo, const uint4 hi, uint32_t& plus, uint32_t& minus) {
+    plus = 0;
+    minus = 0;
+    const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t neg = gather_msb4(v[q]);
+        const uint32_t nz = gather_msb4(nonzero_msb(v[q]));
+        minus |= neg << (4 * q);
+        plus |= (nz & ~neg) << (4 * q);
+    }
+}
 // 32 (or fewer) consecutive int8 sign values -> plus / minus bit words
 // (bit j <-> value j; LSB-first, core.cpp:13-58).  Vector path when the 32
 // values are complete and 16-byte aligned.
