@@ -528,7 +528,8 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
             const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
             if (raw >= 2) {
                 g.f4_st = f4;
-                g.raw_st = raw < H7_MAX_ST ? raw : H7_MAX_ST;
+                static const int raw_max = getenv("LOWBIT_HALO_RAWST") ? atoi(getenv("LOWBIT_HALO_RAWST")) : H7_MAX_ST;
+                g.raw_st = raw < raw_max ? raw : raw_max;  // (tuning knob: LOWBIT_HALO_RAWST caps the raw ring)
                 g.nepi = nepi;
                 g.ok = true;
                 return g;
