@@ -136,9 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                          const HaloParams prm) {
     constexpr int H7_W_CONV = NEPI, H7_W_PROD = H7_W_CONV + H7_NCONV, H7_W_MMA = H7_W_PROD + 1;
     if (prm.dbg & 32768) return;  // launch-overhead probe
-    // programmatic dependent launch: this grid may be launched while the previous kernel
-    // in the stream drains; nothing below reads global memory before that kernel is done
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+
     if ((prm.dbg & 32) && threadIdx.x == 0) atomicMin(&g_halo_phase[0], h7_gtime());
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -203,6 +201,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // programmatic dependent launch: the setup above (barriers, TMEM, the k-block table)
+    // overlaps the previous kernel's tail; global memory is touched only after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[1], h7_gtime());
 
     if (warp == H7_W_PROD) {
@@ -481,6 +482,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
 
     tc_fence_before();
     __syncthreads();
+    // this CTA's work is issued: the next kernel in the stream may begin launching
+    // (its griddepcontrol.wait still waits for this grid to complete)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[2], h7_gtime());
     cluster_sync();
     if (warp == H7_W_MMA) {
