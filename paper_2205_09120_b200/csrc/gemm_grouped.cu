@@ -5,9 +5,9 @@
 // bound on a B200: each problem is 0.4-35 MOPs.  Here every problem's
 // 64 x 32 output tiles are laid out back to back in one grid; a CTA finds its
 // problem with a search over the tile prefix sums in the kernel parameters.
-// The arithmetic is K2's (bit-serial LOP3 + POPC, (nz, sign) form): tiles are
-// small and the operands live in L1/L2, so each thread streams its 4 rows and
-// 4 columns straight from global memory with 128-bit loads.
+// The arithmetic is K2's (bit-serial LOP3 + POPC, (nz, sign) form); a tile's
+// operands (512 depth positions at a time) are staged in shared memory by all
+// its threads at once, so the small tiles pay one L2 latency per chunk.
 #include <cstdio>
 
 #include "common.cuh"
@@ -15,7 +15,7 @@
 
 namespace lb {
 
-constexpr int GR_BM = 64, GR_BN = 32, GR_MAX = 128;
+constexpr int GR_BM = 64, GR_BN = 32, GR_MAX = 128, GR_KQ = 4;  // GR_KQ: 16-byte quads per staged chunk
 
 struct GroupedProblem {
     const uint8_t* a0;
@@ -60,53 +60,78 @@ __global__ void __launch_bounds__(128) gemm_grouped_kernel(const __grid_constant
 
     int acc[4][4] = {};
     int nnz[4] = {0, 0, 0, 0};
-    for (int w0 = 0; w0 < kwords; w0 += 4) {
-        uint32_t as[4][4], an[4][4], bs[4][4], bn[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = row0 + i;
-            uint4 p = make_uint4(0, 0, 0, 0), q = make_uint4(0, 0, 0, 0);
-            if (r < pr.m && w0 < a_words) {
-                p = __ldg(reinterpret_cast<const uint4*>(pr.a0 + (long long)r * pr.a_pitch) + (w0 >> 2));
-                if (A_TER) q = __ldg(reinterpret_cast<const uint4*>(pr.a1 + (long long)r * pr.a_pitch) + (w0 >> 2));
+    // The tile's operands for up to 512 depth positions (16 words) at a time are staged
+    // in shared memory by all threads at once (2-3 16-byte loads each), so a chunk costs
+    // one L2 latency instead of one per 4 words; rows padded to 5 quads (bank spread).
+    __shared__ uint4 sa0[GR_BM][GR_KQ + 1], sa1[GR_BM][GR_KQ + 1], sbs[GR_BN][GR_KQ + 1], sbn[GR_BN][GR_KQ + 1];
+    const int arow0 = tm * GR_BM, bcol0 = tn * GR_BN;
+    for (int wc = 0; wc < kwords; wc += 4 * GR_KQ) {
+        const int nq = (kwords - wc + 3) / 4 < GR_KQ ? (kwords - wc + 3) / 4 : GR_KQ;  // quads in this chunk
+        for (int sl = threadIdx.x; sl < GR_BM * GR_KQ; sl += blockDim.x) {
+            const int r = sl / GR_KQ, q = sl - r * GR_KQ;
+            if (q >= nq) continue;
+            const int w0 = wc + 4 * q;
+            uint4 p = make_uint4(0, 0, 0, 0), pq = make_uint4(0, 0, 0, 0);
+            if (arow0 + r < pr.m && w0 < a_words) {
+                p = __ldg(reinterpret_cast<const uint4*>(pr.a0 + (long long)(arow0 + r) * pr.a_pitch) + (w0 >> 2));
+                if (A_TER) pq = __ldg(reinterpret_cast<const uint4*>(pr.a1 + (long long)(arow0 + r) * pr.a_pitch) + (w0 >> 2));
             }
-            const uint32_t pw[4] = {p.x, p.y, p.z, p.w}, qw[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t msk = tail_mask_word(w0 + j, pr.k);
-                if (A_TER) {
-                    as[i][j] = qw[j] & msk;
-                    an[i][j] = (pw[j] | qw[j]) & msk;
-                } else {
-                    as[i][j] = pw[j] & msk;
-                }
-            }
-            // B: prepared (nz, sign) words, [np][kw] with np >= round_up(n, 256), kw % 8 == 0
-            const long long boff = (long long)(col0 + i) * pr.kw + w0;
-            const uint4 s4 = __ldg(reinterpret_cast<const uint4*>(pr.b_sign + boff));
-            bs[i][0] = s4.x, bs[i][1] = s4.y, bs[i][2] = s4.z, bs[i][3] = s4.w;
-            if (B_TER) {
-                const uint4 n4 = __ldg(reinterpret_cast<const uint4*>(pr.b_nz + boff));
-                bn[i][0] = n4.x, bn[i][1] = n4.y, bn[i][2] = n4.z, bn[i][3] = n4.w;
-            }
+            sa0[r][q] = p;
+            if (A_TER) sa1[r][q] = pq;
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int sl = threadIdx.x; sl < GR_BN * GR_KQ; sl += blockDim.x) {
+            const int c = sl / GR_KQ, q = sl - c * GR_KQ;
+            if (q >= nq) continue;
+            // B: prepared (nz, sign) words, [np][kw] with np >= round_up(n, 256), kw % 8 == 0
+            const long long boff = (long long)(bcol0 + c) * pr.kw + wc + 4 * q;
+            sbs[c][q] = __ldg(reinterpret_cast<const uint4*>(pr.b_sign + boff));
+            if (B_TER) sbn[c][q] = __ldg(reinterpret_cast<const uint4*>(pr.b_nz + boff));
+        }
+        __syncthreads();
+        for (int q = 0; q < nq; ++q) {
+            const int w0 = wc + 4 * q;
+            uint32_t as[4][4], an[4][4], bs[4][4], bn[4][4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                if (MODE == 2) nnz[i] += __popc(an[i][j]);
+                const uint4 p = sa0[ty * 4 + i][q];
+                const uint4 pq = A_TER ? sa1[ty * 4 + i][q] : make_uint4(0, 0, 0, 0);
+                const uint32_t pw[4] = {p.x, p.y, p.z, p.w}, qw[4] = {pq.x, pq.y, pq.z, pq.w};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (MODE == 0) {
-                        acc[i][c] += __popc(as[i][j] ^ bs[c][j]);
-                    } else if (MODE == 1) {
-                        const uint32_t mm = an[i][j] & bn[c][j];
-                        acc[i][c] += __popc(mm) - 2 * __popc(mm & (as[i][j] ^ bs[c][j]));
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t msk = tail_mask_word(w0 + j, pr.k);
+                    if (A_TER) {
+                        as[i][j] = qw[j] & msk;
+                        an[i][j] = (pw[j] | qw[j]) & msk;
                     } else {
-                        acc[i][c] += __popc(an[i][j] & (as[i][j] ^ bs[c][j]));
+                        as[i][j] = pw[j] & msk;
                     }
                 }
+                const uint4 s4 = sbs[tx * 4 + i][q];
+                bs[i][0] = s4.x, bs[i][1] = s4.y, bs[i][2] = s4.z, bs[i][3] = s4.w;
+                if (B_TER) {
+                    const uint4 n4 = sbn[tx * 4 + i][q];
+                    bn[i][0] = n4.x, bn[i][1] = n4.y, bn[i][2] = n4.z, bn[i][3] = n4.w;
+                }
             }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (MODE == 2) nnz[i] += __popc(an[i][j]);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (MODE == 0) {
+                            acc[i][c] += __popc(as[i][j] ^ bs[c][j]);
+                        } else if (MODE == 1) {
+                            const uint32_t mm = an[i][j] & bn[c][j];
+                            acc[i][c] += __popc(mm) - 2 * __popc(mm & (as[i][j] ^ bs[c][j]));
+                        } else {
+                            acc[i][c] += __popc(an[i][j] & (as[i][j] ^ bs[c][j]));
+                        }
+                    }
+                }
+        }
+        __syncthreads();
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
