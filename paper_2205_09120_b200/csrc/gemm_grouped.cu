@@ -8,7 +8,9 @@
 // The arithmetic is K2's (bit-serial LOP3 + POPC, (nz, sign) form); a tile's
 // operands (512 depth positions at a time) are staged in shared memory by all
 // its threads at once, so the small tiles pay one L2 latency per chunk.
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 
 #include "common.cuh"
 #include "layout.cuh"
@@ -159,13 +161,19 @@ extern "C" lowbit_status lowbit_gemm_grouped(int mode, int b_ternary, int count,
                                                        "bnn/tbn a binary one");
     if (count < 0 || (count > 0 && !problems))
         return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "grouped: bad problem list");
+    // deepest problems first: block ids (and with them the SMs the tiles land on)
+    // go round the machine in order of decreasing per-tile cost, which spreads
+    // the K = 512 tiles of config 2 evenly instead of by problem order
+    std::vector<int> order(count);
+    for (int i = 0; i < count; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return problems[x].k > problems[y].k; });
     for (int base = 0; base < count; base += GR_MAX) {
         const int cnt = count - base < GR_MAX ? count - base : GR_MAX;
         GroupedParams P;
         P.count = cnt;
         int tiles = 0;
         for (int i = 0; i < cnt; ++i) {
-            const lowbit_gemm_problem& q = problems[base + i];
+            const lowbit_gemm_problem& q = problems[order[base + i]];
             if (q.m <= 0 || q.n <= 0 || q.k <= 0) return lbhost::set_error(LOWBIT_OUT_OF_BOUNDS, "out of bounds: gemm dims");
             if (q.k > LOWBIT_K_MAX16) {
                 char buf[96];
