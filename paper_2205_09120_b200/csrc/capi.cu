@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "layout.cuh"
+#include "tmap.cuh"
 
 namespace lb {
 lowbit_status launch_bitserial(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
@@ -221,7 +222,13 @@ struct HostCtx {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_in[kChunks] = {}, ev_c[kChunks] = {}, ev_w = nullptr, ev_done = nullptr;
 };
-thread_local HostCtx g_ctx;
+// One context per (host thread, device): scratch, streams and events belong
+// to the device that was current when they were created.
+thread_local HostCtx g_ctx[lb::kMaxDevices];
+HostCtx* host_ctx() {
+    const int dev = lb::current_device();
+    return dev < lb::kMaxDevices ? &g_ctx[dev] : nullptr;
+}
 }  // namespace
 
 extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t* a1, int a_rows,
@@ -239,7 +246,9 @@ extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, co
     const size_t abytes = (size_t)m * pitch;
     const size_t pbytes = lowbit_packed_b_bytes(b_ternary, n, k);
     const size_t wbytes = lowbit_weights_bytes(b_ternary, n, k);
-    HostCtx& X = g_ctx;
+    HostCtx* Xp = host_ctx();
+    if (!Xp) return set_error(LOWBIT_INVALID_ARGUMENT, "host-buffer API: device ordinal out of range");
+    HostCtx& X = *Xp;
     LB_CUDA_TRY(X.a0.ensure(abytes));
     if (a_ternary) LB_CUDA_TRY(X.a1.ensure(abytes));
     LB_CUDA_TRY(X.panels.ensure(pbytes));
@@ -315,7 +324,9 @@ extern "C" lowbit_status lowbit_encode_host(int ternary, const int8_t* values, i
     lowbit_status st;
     if ((st = lowbit_device_check())) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    HostCtx& X = g_ctx;
+    HostCtx* Xp = host_ctx();
+    if (!Xp) return set_error(LOWBIT_INVALID_ARGUMENT, "host-buffer API: device ordinal out of range");
+    HostCtx& X = *Xp;
     const long long sb = (cols + 7) / 8, pitch = lowbit_plane_pitch(cols);
     const size_t vbytes = (size_t)rows * cols, pbytes = (size_t)rows * pitch;
     LB_CUDA_TRY(X.vals.ensure(vbytes));
@@ -344,7 +355,9 @@ extern "C" lowbit_status lowbit_pack_b_host(int ternary, const uint8_t* b0, cons
     lowbit_status st;
     if ((st = lowbit_device_check())) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    HostCtx& X = g_ctx;
+    HostCtx* Xp = host_ctx();
+    if (!Xp) return set_error(LOWBIT_INVALID_ARGUMENT, "host-buffer API: device ordinal out of range");
+    HostCtx& X = *Xp;
     const size_t pbytes = (size_t)k * ((n + 7) / 8);
     const size_t obytes = lowbit_packed_b_bytes(ternary, n, k);
     LB_CUDA_TRY(X.a0.ensure(pbytes));

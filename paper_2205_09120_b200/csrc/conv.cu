@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "encode.cuh"
 #include "layout.cuh"
+#include "tmap.cuh"
 
 namespace lb {
 
@@ -230,12 +231,8 @@ extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int 
     const int wpr = (int)(pitch / 4);
     const long long smem = ((wpr * 4LL + 15) & ~15LL) + (long long)kh * w * c;
     if (c % 32 == 0 && kh < 256 && kw < 256 && smem <= 160 * 1024 && (reinterpret_cast<uintptr_t>(fm) & 15) == 0) {
-        static int attr_bytes = 0;
-        if (smem > 48 * 1024 && smem > attr_bytes) {
-            LB_CUDA_TRY(cudaFuncSetAttribute(conv_encode_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
-            attr_bytes = (int)smem;
-        }
+        static SmemOptIn attr;
+        if (smem > 48 * 1024) LB_CUDA_TRY(attr.ensure(conv_encode_rows_kernel, (int)smem));
         const long long orows = (long long)batch * g.oh;
         const int blocks = (int)(orows < 148LL * 8 ? orows : 148LL * 8);
         conv_encode_rows_kernel<<<blocks, 256, (size_t)smem, (cudaStream_t)stream>>>(a_binary, fm, g, pad_value,
@@ -339,7 +336,10 @@ struct ConvScratch {
         return e;
     }
 };
-thread_local ConvScratch g_fm, g_ws, g_pan, g_w, g_out, g_out32, g_flag;
+struct ConvHostCtx {
+    ConvScratch fm, ws, pan, w, out, out32, flag;
+};
+thread_local ConvHostCtx g_conv_ctx[kMaxDevices];  // per (host thread, device)
 }  // namespace
 
 extern "C" lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
@@ -354,6 +354,11 @@ extern "C" lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batc
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
     const size_t fm_bytes = (size_t)batch * h * w * c;
     const size_t pbytes = lowbit_packed_b_bytes(b_ternary, cout, k);
+    const int dev = current_device();
+    if (dev >= kMaxDevices) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d_host: device ordinal out of range");
+    ConvHostCtx& X = g_conv_ctx[dev];
+    ConvScratch &g_fm = X.fm, &g_ws = X.ws, &g_pan = X.pan, &g_w = X.w, &g_out = X.out, &g_out32 = X.out32,
+                &g_flag = X.flag;
     LB_CUDA_TRY(g_fm.ensure(fm_bytes + 16));
     LB_CUDA_TRY(g_ws.ensure(lowbit_conv2d_workspace_bytes(mode, batch, h, w, c, kh, kw, stride, padding)));
     LB_CUDA_TRY(g_pan.ensure(pbytes));

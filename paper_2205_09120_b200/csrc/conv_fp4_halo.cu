@@ -609,11 +609,8 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     if (!make_map_nhwc_box(&mraw, fm, batch, h, w, cch, (uint32_t)g.P, (uint32_t)g.rows_h))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the feature-map halo");
     auto kern = g.nepi == 16 ? conv_fp4_halo_kernel<16> : conv_fp4_halo_kernel<8>;
-    static bool attr[2] = {false, false};
-    if (!attr[g.nepi == 16]) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H7_SMEM));
-        attr[g.nepi == 16] = true;
-    }
+    static SmemOptIn attr[2];
+    LB_CUDA_TRY(attr[g.nepi == 16].ensure(kern, H7_SMEM));
     const int pairs = prm.ptiles < num_sms() / 2 ? prm.ptiles : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);

@@ -583,13 +583,14 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
     const bool tl = halo_ok(batch, h, w, cch, cout, kh, kw, stride, pad) && !no_tl;
     const int hp = h + 2 * pad, wp = halo_pitch(w, pad);
     uint8_t* fm4 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 1023) & ~uintptr_t(1023));
-    static bool carve = false;
-    if (!carve) {  // run the pack passes with K6's shared-memory carveout: no L1/smem reconfiguration between them
+    static bool carve[kMaxDevices] = {};
+    const int cdev = current_device();
+    if (cdev >= kMaxDevices || !carve[cdev]) {  // run the pack passes with K6's shared-memory carveout: no L1/smem reconfiguration between them
         cudaFuncSetAttribute(conv_pack_fp4_padded_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(conv_pack_fp4_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        carve = true;
+        if (cdev < kMaxDevices) carve[cdev] = true;
     }
     if (tl) {
         const int prows = batch * hp;
@@ -656,12 +657,8 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
                                 make_map_2d(&mc64, out, (uint64_t)cout, (uint64_t)rows, (uint64_t)cout * 2, 64, 32,
                                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_UINT16);
     if (!mc_ok) return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv output");
-    static bool attr[2] = {false, false};
-    if (!attr[tl]) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(tl ? conv_fp4_pair_kernel<true> : conv_fp4_pair_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C6_SMEM));
-        attr[tl] = true;
-    }
+    static SmemOptIn attr[2];
+    LB_CUDA_TRY(attr[tl].ensure(tl ? conv_fp4_pair_kernel<true> : conv_fp4_pair_kernel<false>, C6_SMEM));
     const int pairs = prm.m_tiles < num_sms() / 2 ? prm.m_tiles : num_sms() / 2;
     if (tl) conv_fp4_pair_kernel<true><<<2 * pairs, C6_THREADS, C6_SMEM, stream>>>(mb, ma, mc, mc64, prm);
     else conv_fp4_pair_kernel<false><<<2 * pairs, C6_THREADS, C6_SMEM, stream>>>(mb, ma, mc, mc64, prm);

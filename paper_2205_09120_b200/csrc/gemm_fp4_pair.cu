@@ -772,20 +772,17 @@ static int pick_bn_fp4(int n, int max_bn = F4_MAX_BN) {
 template <bool A_TER, bool AR, int LAYOUT, int CL = 2>
 static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                         const CUtensorMap& mc, const Fp4Params& prm, int pairs, cudaStream_t stream) {
-    static bool attr = false;
+    static SmemOptIn attr;
     static int max_clusters = 0;
     constexpr int smem = f4_smem_bytes(AR);
     auto kern = gemm_fp4_pair_kernel<A_TER, AR, LAYOUT, CL>;
-    if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        if (CL == 4) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(4 * 37);
-            cfg.blockDim = dim3(F4_THREADS);
-            cfg.dynamicSmemBytes = smem;
-            LB_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
-        }
-        attr = true;
+    LB_CUDA_TRY(attr.ensure(kern, smem));
+    if (CL == 4 && !max_clusters) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(4 * 37);
+        cfg.blockDim = dim3(F4_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        LB_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
     }
     int grid = 2 * pairs;
     if (CL == 4) {  // whole clusters, all co-resident (a later wave would serialise the lockstep pairs)

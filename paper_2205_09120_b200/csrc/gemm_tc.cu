@@ -215,12 +215,8 @@ static int pick_bn(int n) {
 template <bool A_TER, int LAYOUT>
 static lowbit_status launch_tc_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                        const TcParams& prm, int grid, cudaStream_t stream) {
-    static bool attr = false;
-    if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<A_TER, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         TC_SMEM_BYTES));
-        attr = true;
-    }
+    static SmemOptIn attr;
+    LB_CUDA_TRY(attr.ensure(gemm_tc_kernel<A_TER, LAYOUT>, TC_SMEM_BYTES));
     gemm_tc_kernel<A_TER, LAYOUT><<<grid, TC_THREADS, TC_SMEM_BYTES, stream>>>(mb, ma0, ma1, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;

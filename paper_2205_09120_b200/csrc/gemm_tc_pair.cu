@@ -410,12 +410,8 @@ static int pick_bn_pair(int n) {
 template <bool A_TER, int LAYOUT>
 static lowbit_status launch_pair_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                          const CUtensorMap& mc, const PairParams& prm, int pairs, cudaStream_t stream) {
-    static bool attr = false;
-    if (!attr) {
-        LB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_pair_kernel<A_TER, LAYOUT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, PR_SMEM_LIMIT));
-        attr = true;
-    }
+    static SmemOptIn attr;
+    LB_CUDA_TRY(attr.ensure(gemm_tc_pair_kernel<A_TER, LAYOUT>, PR_SMEM_LIMIT));
     const int smem = pr_smem_bytes(prm.a_stages, prm.b_stages, prm.raw_stages);
     gemm_tc_pair_kernel<A_TER, LAYOUT><<<2 * pairs, PR_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
     LB_CUDA_TRY(cudaGetLastError());

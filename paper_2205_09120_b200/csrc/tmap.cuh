@@ -98,15 +98,45 @@ inline bool make_map_im2col(CUtensorMap* map, const void* base, int n, int h, in
     return r == CUDA_SUCCESS;
 }
 
-inline int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
 }
+
+constexpr int kMaxDevices = 64;
+
+// SM count of the current device (cached per device: one process may drive
+// several GPUs from different host threads).
+inline int num_sms() {
+    static int sms[kMaxDevices] = {};
+    const int dev = current_device();
+    if (dev >= kMaxDevices) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }
+    if (!sms[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        sms[dev] = n > 0 ? n : 148;
+    }
+    return sms[dev];
+}
+
+// Largest dynamic-shared-memory opt-in already applied to one kernel, per
+// device (cudaFuncSetAttribute is per device).  ensure() sets the attribute
+// the first time a device needs `bytes` or more.
+struct SmemOptIn {
+    int bytes[kMaxDevices] = {};
+    template <typename K>
+    cudaError_t ensure(K kern, int need) {
+        const int dev = current_device();
+        if (dev < kMaxDevices && bytes[dev] >= need) return cudaSuccess;
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+        if (e == cudaSuccess && dev < kMaxDevices) bytes[dev] = need;
+        return e;
+    }
+};
 
 }  // namespace lb
