@@ -214,6 +214,32 @@ def test_host_dropin_entry(lb, port, ref):
         assert (got == ref.gemm(mode, a, b)).all()
 
 
+def test_host_dropin_threads(lb, port, ref):
+    # host-buffer calls from several host threads at once: each thread owns its
+    # scratch, streams and events (thread_local per device in capi.cu)
+    from concurrent.futures import ThreadPoolExecutor
+    cases = []
+    for i, (mode, (m, n, k)) in enumerate([(TNN, (300, 96, 512)), (TBN, (129, 64, 300)),
+                                           (BNN, (64, 200, 1024)), (TNN, (1000, 32, 128))]):
+        da, db = mode_dists(mode)
+        a = port.generate(da, 90 + i, 0, m, k)
+        b = port.generate(db, 90 + i, 1, k, n)
+        a0, a1 = port.encode(a, a_mode_ternary(mode))
+        b0, b1 = port.encode(b, b_mode_ternary(mode))
+        cases.append((mode, m, n, k, a0, a1, port.pack_b(b0, b1, k, n), b1 is not None, ref.gemm(mode, a, b)))
+
+    def run(case):
+        mode, m, n, k, a0, a1, panels, bt, want = case
+        for _ in range(5):
+            got = lb.gemm_lowbit_host(mode, a0, a1, m, k, panels, bt, n, k, (m, n, k))
+            if not (got == want).all():
+                return False
+        return True
+
+    with ThreadPoolExecutor(len(cases)) as ex:
+        assert all(ex.map(run, cases))
+
+
 # ------------------------------------------------------------------ BASELINE configs
 def _device_inputs(lb, mode, seed, m, n, k, dist_a, dist_b):
     a = lb.generate(dist_a, seed, 0, m, k)
