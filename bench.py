@@ -163,44 +163,137 @@ def load_traffic():
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref) on a bounded sample
+# CPU reference (oracle/_ref) on bounded samples — BASELINE.md §2
 # ---------------------------------------------------------------------------
-def reference_cpu_rate(cfg_name, target_s=8.0, threads=None):
-    from oracle.oracle import Port, Ref, a_mode_ternary, b_mode_ternary
-    mode, M, N, K, da, db, seed = CONFIGS[cfg_name]
-    port = Port()
-    kind = "reference" if Ref.available() else "port"
-    if kind != "reference":
-        return None
-    ref = Ref()
-    threads = threads or os.cpu_count() or 1
-    b = port.generate(db, seed, 1, K, N)
+def _ref_lib(native=False):
+    from oracle.oracle import REF_NATIVE_SO, REF_SO, Ref
+    path = REF_NATIVE_SO if native else REF_SO
+    return Ref(path) if Ref.available(path) else None
+
+
+def cpu_gemm(ref, port, mode, M, N, K, da, db, seed, ids=(0, 1), threads=1, rows=None, target_s=None, reps=1,
+             from_i8=False):
+    """The reference gemm_lowbit (oracle/_ref, built from /root/reference/proj/src) on `rows` rows of a
+    config, split over `threads` contiguous row shards (one std::thread each; the library is pure,
+    kernels.cpp:23).  Policy of bench.cpp:214-233: one warm-up run, then the median of `reps` timed
+    runs; encode(A) and pack_b excluded — unless from_i8, which times encode_* + gemm_lowbit ("from
+    int8 A").  target_s: grow the row sample until one run takes ~target_s."""
+    from oracle.oracle import a_mode_ternary, b_mode_ternary
+    b = port.generate(db, seed, ids[1], K, N)
     b0, b1 = ref.encode(b, b_mode_ternary(mode))
 
-    def run(rows, reps=1):
-        rows = min(rows, M)
-        a = port.generate(da, seed, 0, rows, K)
-        a0, a1 = ref.encode(a, a_mode_ternary(mode))
-        h = ref.bench_prepare(mode, a0, a1, rows, K, b0, b1, N, threads)
+    def run(r, reps_):
+        r = min(r, M)
+        a = port.generate(da, seed, ids[0], r, K)
+        if from_i8:
+            h = ref.bench_prepare_i8(mode, a, r, K, b0, b1, N, threads)
+        else:
+            a0, a1 = ref.encode(a, a_mode_ternary(mode))
+            h = ref.bench_prepare(mode, a0, a1, r, K, b0, b1, N, threads)
         ref.bench_run(h)  # warm-up (bench.cpp:214)
         ts = []
-        for _ in range(reps):
+        for _ in range(reps_):
             t0 = time.perf_counter()
             ref.bench_run(h)
             ts.append(time.perf_counter() - t0)
         ref.bench_free(h)
-        return rows, float(np.median(ts))
+        return r, float(np.median(ts))
 
-    rows, t = run(max(threads, 16))
-    while t < 0.5 and rows < M:  # calibrate: thread start-up dominates tiny samples
-        rows, t = run(min(M, rows * 4))
-    ops_rate = 2.0 * rows * N * K / t
-    rows = int(min(M, max(rows, target_s * ops_rate / (2.0 * N * K))))
-    rows, t = run(rows)
-    return {"value": 2.0 * rows * N * K / t / 1e12, "unit": "TOPS", "cores": threads, "kind": kind,
-            "sample": f"{MODE_NAME[mode]} {rows} x {N} x {K} rows of {cfg_name} (gemm_lowbit on {threads} "
-                      f"row shards, encode/pack_b excluded, median after warm-up), {t:.2f} s",
-            "seconds": t}
+    if target_s is not None:
+        # calibrate on whole 16-row tiles per shard (gemm_lowbit pads row blocks to 16, kernels.hpp:27);
+        # thread start-up dominates tiny samples
+        r, t = run(64 * threads, 1)
+        while t < 0.2 * target_s and r < M:
+            r, t = run(min(M, r * 4), 1)
+        rows = int(min(M, max(r, target_s * r / t)))
+    rows, t = run(rows or M, reps)
+    return {"rows": rows, "seconds": t, "TOPS": 2.0 * rows * N * K / t / 1e12}
+
+
+def reference_cpu_rate(cfg_name, target_s=8.0, threads=None, native=False, one_core_s=None):
+    """Bounded-sample rate of the reference CPU path on config `cfg_name` at `threads` (default: all
+    host threads), as a cpu_baseline object.  one_core_s: also a 1-thread figure on ~that many s."""
+    from oracle.oracle import Port
+    mode, M, N, K, da, db, seed = CONFIGS[cfg_name]
+    ref = _ref_lib(native)
+    if ref is None:
+        return None
+    port = Port()
+    threads = threads or os.cpu_count() or 1
+    r = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=threads, target_s=target_s)
+    out = {"value": r["TOPS"], "unit": "TOPS", "cores": threads, "kind": "reference",
+           "sample": f"{MODE_NAME[mode]} {r['rows']} x {N} x {K} rows of {cfg_name} (gemm_lowbit on {threads} "
+                     f"row shards, encode/pack_b excluded, warm-up then timed), {r['seconds']:.2f} s",
+           "seconds": r["seconds"], "build": "x86-64-v3" if native else "reference flags (-O3)"}
+    if one_core_s:
+        r1 = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=1, target_s=one_core_s)
+        out["one_core"] = {"value": r1["TOPS"], "cores": 1, "sample": f"{r1['rows']} rows, {r1['seconds']:.2f} s"}
+    return out
+
+
+def cpu_baselines(threads=None):
+    """BASELINE.md §2 beside every GPU number: the reference CPU path on this host for configs 1-5,
+    on all host threads and on 1 core, its own -O3 build and the x86-64-v3 build, plus the
+    "from int8 A" line (encode included).  Bounded samples; ~1 min in total."""
+    from oracle.oracle import Port
+    port = Port()
+    threads = threads or os.cpu_count() or 1
+    out = {}
+    for native in (False, True):
+        ref = _ref_lib(native)
+        if ref is None:
+            continue
+        tag = "x86_64_v3" if native else "reference_build"
+        # c1: the whole config, median of 5, 1 core (the reference bench's own policy)
+        mode, M, N, K, da, db, seed = CONFIGS["c1"]
+        r = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=1, reps=5)
+        ri = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=1, reps=5, from_i8=True)
+        out.setdefault("c1", {})[tag] = {
+            "value": r["TOPS"], "unit": "TOPS", "cores": 1, "kind": "reference", "ms": r["seconds"] * 1e3,
+            "from_int8": {"value": ri["TOPS"], "ms": ri["seconds"] * 1e3},
+            "sample": "whole config, median of 5 after one warm-up (bench.cpp:214-233)"}
+        # c2: the 64-shape TBN sweep, sum of the 64 medians, 1 core
+        tot = tot_i8 = 0.0
+        ops = 0.0
+        for sidx, (m, n, k) in enumerate(SWEEP):
+            r = cpu_gemm(ref, port, 2, m, n, k, 2, 1, 44, ids=(2 * sidx, 2 * sidx + 1), threads=1, reps=5)
+            ri = cpu_gemm(ref, port, 2, m, n, k, 2, 1, 44, ids=(2 * sidx, 2 * sidx + 1), threads=1, reps=5,
+                          from_i8=True)
+            tot += r["seconds"]
+            tot_i8 += ri["seconds"]
+            ops += 2.0 * m * n * k
+        out.setdefault("c2", {})[tag] = {
+            "value": ops / tot / 1e12, "unit": "TOPS", "cores": 1, "kind": "reference", "ms_64_shapes": tot * 1e3,
+            "from_int8": {"value": ops / tot_i8 / 1e12, "ms_64_shapes": tot_i8 * 1e3},
+            "sample": "all 64 shapes, sum of medians of 5 (bench.cpp:196-234)"}
+        # c3, c5: row samples on all threads and on 1 core
+        for name, ts, t1 in (("c3", 3.0, 1.5), ("c5", 4.0, 1.5)):
+            mode, M, N, K, da, db, seed = CONFIGS[name]
+            r = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=threads, target_s=ts)
+            r1 = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=1, target_s=t1)
+            ri = cpu_gemm(ref, port, mode, M, N, K, da, db, seed, threads=threads, rows=r["rows"], from_i8=True)
+            out.setdefault(name, {})[tag] = {
+                "value": r["TOPS"], "unit": "TOPS", "cores": threads, "kind": "reference",
+                "sample": f"{r['rows']} of {M} rows on {threads} row shards, {r['seconds']:.2f} s",
+                "one_core": {"value": r1["TOPS"], "cores": 1, "sample": f"{r1['rows']} rows, {r1['seconds']:.2f} s"},
+                "from_int8": {"value": ri["TOPS"], "cores": threads, "sample": f"{ri['rows']} rows"}}
+        # c4: 64 single-image conv2d_lowbit calls (im2col + encode + pack_b + gemm, conv.cpp:33-59):
+        # a sample of the batch's images, extrapolated to all 64
+        ops4 = 2.0 * 200704 * 128 * 1152
+        wt = port.generate(0, 46, 1, 9 * 128, 128)
+        c4 = {}
+        for thr, imgs in ((threads, min(64, 2 * threads)), (1, 2)):
+            fm = port.generate(0, 46, 0, imgs * 56 * 56, 128).reshape(imgs, 56, 56, 128)
+            ref.bench_conv(1, fm[:1], False, wt, False, 3, 3, 1, 1, 1)  # warm-up
+            t0 = time.perf_counter()
+            ref.bench_conv(1, fm, False, wt, False, 3, 3, 1, 1, thr)
+            dt = time.perf_counter() - t0
+            t64 = dt * 64.0 / imgs
+            c4[thr] = {"value": ops4 / t64 / 1e12, "cores": thr, "ms_64_images": t64 * 1e3,
+                       "sample": f"{imgs} of 64 images as single-image conv2d_lowbit calls on {thr} thread(s), "
+                                 f"{dt:.2f} s"}
+        out.setdefault("c4", {})[tag] = dict(c4[threads], unit="TOPS", kind="reference", one_core=c4[1])
+    return out
 
 
 def run_reference_arm(args):
@@ -245,10 +338,10 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "tensor", "tensor_i8", "bitserial"])
-    ap.add_argument("--layout", default="nibbles", choices=["nibbles", "lanes", "reference"],
-                    help="A plane layout written by the (untimed) encode: nibbles -> fp4 (kind::mxf4) tensor-core "
-                         "kernel K5, lanes -> int8 (kind::i8) kernel K3, reference (the reference's own bit order) "
-                         "-> K5 for large shapes, K3 for launch-bound ones")
+    ap.add_argument("--layout", default="reference", choices=["nibbles", "lanes", "reference"],
+                    help="A plane layout written by the (untimed) encode: reference (the reference's own bit "
+                         "order, what the drop-in API exchanges) -> fp4 (kind::mxf4) K5 for large shapes, K3 for "
+                         "launch-bound ones; nibbles -> K5; lanes -> int8 (kind::i8) K3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-config side measurements")
@@ -270,7 +363,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    # under torchrun (even at N = 1) the ranks form an NCCL group: barriers, the max-over-ranks
+    # reduction and the output gather run exactly as at N = 8
+    distributed = world > 1 or "LOCAL_RANK" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     kernel = {"auto": lb.KERNEL_AUTO, "tensor": lb.KERNEL_TENSOR, "tensor_i8": lb.KERNEL_TENSOR_I8,
               "bitserial": lb.KERNEL_BITSERIAL}[args.kernel]
@@ -303,7 +399,7 @@ def main():
         flush_l2(flush)
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -314,13 +410,13 @@ def main():
             step()
             ev[i][1].record()
         torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in ev]
     my_ms = float(np.sum(step_ms))
     t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -356,7 +452,7 @@ def main():
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier()
         es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         es.record()
@@ -365,7 +461,7 @@ def main():
         ee.record()
         torch.cuda.synchronize()
         te = torch.tensor([es.elapsed_time(ee) / e2e_steps], dtype=torch.float64, device="cuda")
-        if world > 1:
+        if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         h2d = h_a0.numel() + (h_a1.numel() if h_a1 is not None else 0) + h_pan.numel()
         e2e = {"value": ops_total / (te.item() * 1e-3) / 1e12, "unit": "TOPS",
@@ -374,11 +470,35 @@ def main():
                                                  "int16 C out; includes B upload + prepare per call)"}
         # sanity: e2e output equals the device-resident output
         assert torch.equal(h_c.cuda(), c), "e2e output differs from device path"
+        # the same call with PAGEABLE host buffers (numpy arrays, as most callers hold them): the
+        # library stages them through pinned slots on a few host threads
+        if world == 1:
+            p_a0 = h_a0.numpy().copy()
+            p_a1 = h_a1.numpy().copy() if h_a1 is not None else None
+            p_pan = h_pan.numpy().copy()
+            p_c = np.zeros((m, N), np.int16)  # pre-touched, like a reused output buffer
+
+            def e2e_pageable():
+                lb.gemm_lowbit_host(mode, p_a0, p_a1, m, K, p_pan, mode == 1, N, K, (m, N, K), kernel=kernel,
+                                    out=p_c)
+            e2e_pageable()
+            ts = []
+            for _ in range(e2e_steps):
+                t0 = time.perf_counter()
+                e2e_pageable()
+                ts.append(time.perf_counter() - t0)
+            assert np.array_equal(p_c, h_c.numpy()), "pageable e2e output differs"
+            tp = float(np.mean(ts))
+            e2e["pageable"] = {"value": ops_total / tp / 1e12, "unit": "TOPS", "ms_per_step": tp * 1e3,
+                               "path": "lowbit_gemm_lowbit_host with pageable (numpy) host buffers, host clock "
+                                       "around the synchronous call"}
+            del p_a0, p_a1, p_pan, p_c
+            e2e["cpp_dropin"] = cpp_dropin_e2e(mode, M, N, K, seed)
         del h_a0, h_a1, h_c
         ap_ref = None
 
     gather = None
-    if world > 1 and not args.no_gather:
+    if distributed and not args.no_gather:
         # NCCL output gather to rank 0 (only where a consumer needs the whole C;
         # not part of `value`): int16 shards travel as bytes
         from paper_2205_09120_b200.shard import gather_rows
@@ -427,15 +547,21 @@ def main():
                 "peak_source": "148 SMs x 16 POPC/clk x 32 bits x 2 ops x max clock (TNN: 2 POPC per word)"}
 
     cpu = None
+    cpu_all = {}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = reference_cpu_rate(args.config)
+            cpu_all = cpu_baselines()
+            cpu = dict(cpu_all[args.config]["reference_build"])
+            if "x86_64_v3" in cpu_all[args.config]:
+                cpu["x86_64_v3"] = cpu_all[args.config]["x86_64_v3"]
         except Exception as e:  # never let the baseline break the bench line
-            cpu = {"value": None, "error": str(e)}
+            cpu = {"value": None, "error": repr(e)}
 
     extra = {}
     if rank == 0 and world == 1 and not args.no_extra:
         extra = side_configs(lb, torch, flush, pk)
+    for name, cb in cpu_all.items():  # the reference CPU path beside every GPU number
+        extra.setdefault(name, {})["cpu_baseline"] = cb
 
     if rank == 0:
         line = {
@@ -444,7 +570,9 @@ def main():
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": ("u8 bit-planes in, packed e2m1 (fp4) tensor-core MMA with unit block scales, f32 accumulate "
                       "(exact: |partial sums| <= 32767), int16 out" if fp4 else
-                      "u8 bit-planes in, int8 tensor-core MMA, int32 accumulate, int16 out"),
+                      "u8 bit-planes in, int8 tensor-core MMA, int32 accumulate, int16 out"
+                      if chosen in (lb.KERNEL_TENSOR, lb.KERNEL_TENSOR_I8, lb.KERNEL_TENSOR_1CTA) else
+                      "u8 bit-planes in, LOP3 + POPC, int32 accumulate, int16 out"),
             "data": "synthetic (counter-based splitmix64 generator, BASELINE.json distributions)",
             "config": {"workload": f"{args.config}: {MODE_NAME[mode]} GeMM M={M} N={N} K={K} int16 C, "
                                    f"A rows sharded over {world} GPU(s), B replicated",
@@ -453,14 +581,38 @@ def main():
                                   4: "tensor (int8 K3)"}.get(chosen, str(chosen)),
                        "a_layout": {2: "nibbles (B200 nibble-interleaved bit planes from K1)",
                                     1: "lanes (B200 lane-interleaved bit planes from K1)",
-                                    0: "reference"}[layout],
+                                    0: "reference (the reference's own plane encoding, core.hpp:3-10: what "
+                                       "the drop-in API hands the library)"}[layout],
                        "parallelism": f"row-shard x{world}"},
             "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "gather": gather, "per_config": extra,
         }
         print(json.dumps(line))
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
+
+
+def cpp_dropin_e2e(mode, M, N, K, seed, iters=3):
+    """End to end through the C++ drop-in exactly as a reference caller uses it: std::vector planes
+    in, `Int16Matrix c = lowbit::gemm_lowbit(...)` out (cpp/bench/dropin_e2e.cpp; host clock around
+    each call, result allocation included — the reference allocates it too, gemm.cpp:79-112)."""
+    exe = os.path.join(ROOT, "paper_2205_09120_b200", "cpp", "build", "dropin_e2e")
+    if not os.path.exists(exe):
+        return {"unavailable": "cpp/build/dropin_e2e not built"}
+    try:
+        r = subprocess.run([exe, str(mode), str(M), str(N), str(K), str(iters), str(seed)], capture_output=True,
+                           text=True, timeout=600)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not line:
+            return {"error": f"rc={r.returncode} {r.stderr[-300:]}"}
+        d = json.loads(line[-1])
+        return {"value": d["TOPS"], "unit": "TOPS", "ms_per_step": d["ms_mean"],
+                "h2d_bytes_per_step": d["h2d_bytes_per_call"], "d2h_bytes_per_step": d["d2h_bytes_per_call"],
+                "equal_device_path": d["equal_device_path"],
+                "path": "C++ drop-in lowbit::gemm_lowbit(mode, TernaryPackedMatrix, PackedB, dims) -> Int16Matrix, "
+                        "std::vector buffers, host clock, result allocation included"}
+    except Exception as e:
+        return {"error": repr(e)}
 
 
 def flush_l2(flush):
@@ -543,6 +695,9 @@ def side_configs(lb, torch, flush, pk):
     """BASELINE.json configs 1-4 at N=1: device time per kernel, TOPS and the
     fraction of the binding roofline.  Small configs (c1, c2) are timed as
     CUDA-graph replays (launch-latency bound); c3/c4 with events + L2 flush."""
+    import ctypes as C
+    L = lb._lib
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     out = {}
     tensor_peak = 2.0 * pk["bf16_tflops"]
     popc = lambda mode: 148 * 16 * 32 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 / (2 if mode == 1 else 1)
@@ -573,6 +728,21 @@ def side_configs(lb, torch, flush, pk):
                        "bound": "popc" if kn == "bitserial" else "tensor"}
         res["auto"] = {2: "tensor_fp4", 3: "tensor_1cta (int8, single-CTA; reference planes)",
                        4: "tensor_i8 (reference planes)"}.get(lb.select_kernel(mode, M, N, K))
+        # "from int8 A" (BASELINE.md §2 second line): the sign matrix in HBM, encode included
+        pl = lb.empty_planes(M, K, mode != 0)
+
+        def enc_gemm():
+            L.check(L.lib.lowbit_encode_ex(int(mode != 0), 0, C.c_void_p(a.data_ptr()), M, K, K,
+                                           C.c_void_p(pl.plane0.data_ptr()),
+                                           C.c_void_p(pl.plane1.data_ptr()) if pl.plane1 is not None else None,
+                                           pl.pitch, None, st), "encode")
+            lb.gemm_lowbit(mode, pl, w, (M, N, K), out=c)
+        for kn, f in (("from_int8_encode_then_auto", enc_gemm),
+                      ("from_int8_gemm_i8", lambda: lb.gemm_lowbit_i8(mode, a, w, (M, N, K), out=c))):
+            ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
+            res[kn] = {"ms": ms, "TOPS": 2.0 * M * N * K / (ms * 1e-3) / 1e12}
+        res["from_int8_encode_then_auto"]["path"] = "K1 encode (reference planes) + lowbit_gemm AUTO: two launches"
+        res["from_int8_gemm_i8"]["path"] = "lowbit_gemm_i8: int8 A by TMA straight into tcgen05 kind::i8"
         res["timing"] = "cuda graph replay" if name == "c1" else "events, L2 flushed"
         out[name] = res
     # c2: the 64-shape TBN sweep (one launch per shape), captured as one graph
@@ -594,6 +764,18 @@ def side_configs(lb, torch, flush, pk):
     probs = [(aps[s], ws[s], cs[s]) for s in range(len(SWEEP))]
     ms = graph_time(torch, lambda: lb.gemm_grouped(2, probs), reps=20)
     res["grouped_one_launch"] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12}
+    # from int8 A: the 64 encodes (one launch each) + the grouped GeMM launch, one graph
+    a8 = [lb.generate(2, 44, 2 * s, M, K) for s, (M, N, K) in enumerate(SWEEP)]
+
+    def sweep_i8():
+        for s, (M, N, K) in enumerate(SWEEP):
+            L.check(L.lib.lowbit_encode_ex(1, 0, C.c_void_p(a8[s].data_ptr()), M, K, K,
+                                           C.c_void_p(aps[s].plane0.data_ptr()), C.c_void_p(aps[s].plane1.data_ptr()),
+                                           aps[s].pitch, None, st), "encode")
+        lb.gemm_grouped(2, probs)
+    ms = graph_time(torch, sweep_i8, reps=20)
+    res["from_int8_grouped"] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12,
+                                "path": "64 K1 encodes + one grouped bit-serial launch, one graph"}
     res["timing"] = "cuda graph (64 launches, or 1 grouped launch), replayed"
     out["c2"] = res
     # c4: conv 64x56x56x128, 3x3 -> 128, s1 p1 (K4 fused im2col+encode + GeMM)
@@ -630,9 +812,6 @@ def side_configs(lb, torch, flush, pk):
     pitch = lb.plane_pitch(1152)
     p0 = wsp[: 200704 * pitch]
     p1 = wsp[200704 * pitch: 2 * 200704 * pitch]
-    L = lb._lib
-    import ctypes as C
-    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     k4 = lambda: L.check(L.lib.lowbit_conv_encode(0, C.c_void_p(fm.data_ptr()), 64, 56, 56, 128, 3, 3, 1, 1, 0,
                                                   C.c_void_p(p0.data_ptr()), C.c_void_p(p1.data_ptr()), pitch,
                                                   None, st))
@@ -662,7 +841,18 @@ def side_configs(lb, torch, flush, pk):
     out["c5_from_int8_via_fp4"] = {"ms": ms, "TOPS": ops5 / (ms * 1e-3) / 1e12,
                                    "frac": ops5 / (ms * 1e-3) / 1e12 / fp4_peak,
                                    "path": "K1 encode (NIBBLES planes, HBM-bound) + K5 fp4 GeMM"}
-    del c5, w5
+    # K2 (bit-serial, LOP3 + POPC) on c5: north_star's primary kernel on the largest TNN shape
+    p5 = lb.encode_ternary(a)
+    ms = time_device(torch, lambda: lb.gemm_lowbit(1, p5, w5, (1048576, 1024, 2048), kernel=lb.KERNEL_BITSERIAL,
+                                                   out=c5), flush, reps=3)
+    out["c5_bitserial"] = {"ms": ms, "TOPS": ops5 / (ms * 1e-3) / 1e12, "frac": ops5 / (ms * 1e-3) / 1e12 / popc(1),
+                           "bound": "popc", "path": "K2 gemm_bitserial_kernel on reference planes"}
+    del p5
+    p5 = lb.encode_ternary(a, layout=2)
+    ms = time_device(torch, lambda: lb.gemm_lowbit(1, p5, w5, (1048576, 1024, 2048), out=c5), flush, reps=10)
+    out["c5_fp4_nibbles"] = {"ms": ms, "TOPS": ops5 / (ms * 1e-3) / 1e12, "frac": ops5 / (ms * 1e-3) / 1e12 / fp4_peak,
+                             "path": "K5 on NIBBLES planes (canonical fp4 B section)"}
+    del p5, c5, w5
     # K1 encode of c5's A (HBM-bound): 2 GiB int8 in, 2 x 512 MiB planes out
     eb = 1048576 * 2048 + 2 * 1048576 * planes.pitch
     for lay, name in ((2, "k1_encode_c5_nibbles"), (1, "k1_encode_c5_lanes"), (0, "k1_encode_c5_reference_layout")):

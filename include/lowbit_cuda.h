@@ -190,7 +190,11 @@ lowbit_status lowbit_gemm_grouped(int mode, int b_ternary, int count, const lowb
 /* ---- host-buffer drop-in: one whole reference gemm_lowbit call -----------
  * Host A planes with the reference stride ceil(a_cols/8); host PackedB
  * panels; host C (m x n, row-major).  Uploads, prepares B, runs, downloads
- * and synchronises `stream`.  Device scratch is cached per host thread. */
+ * and synchronises `stream`.  Host buffers may be pinned or pageable
+ * (pageable ones are staged through pinned slots).  Device scratch, copy
+ * streams and staging slots are cached per (host thread, device) and freed
+ * when the thread exits or by lowbit_release_thread_state().  On any error
+ * the call has finished all of its copies before it returns. */
 lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t* a1, int a_rows, int a_cols,
                                       const uint8_t* panels, int b_ternary, int b_n, int b_k, int m, int n, int k,
                                       int k_blk, int16_t* c, int kernel, lowbit_stream stream);
@@ -239,6 +243,11 @@ lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, int h, int w,
 lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
                                  const uint8_t* panels, int b_ternary, int cout, int k, int kh, int kw, int stride,
                                  int padding, int binary_pad_value, int32_t* out, lowbit_stream stream);
+
+/* Free this host thread's cached host-buffer state on every device
+ * (device scratch, pinned staging, streams, events).  Optional: the same
+ * happens when the thread exits.  The next host-buffer call re-creates it. */
+void lowbit_release_thread_state(void);
 
 /* ---- host-buffer forms of K1 / K1b (used by the C++ drop-in) -------------
  * Host planes use the reference stride ceil(cols/8) bytes.  Synchronous. */

@@ -22,6 +22,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liblowbit_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "liblowbit_ref.so")
+# the same reference sources built with -march=x86-64-v3 (BASELINE.md §2's second CPU line)
+REF_NATIVE_SO = os.path.join(HERE, "_ref", "liblowbit_ref_native.so")
 
 BNN, TNN, TBN = 0, 1, 2
 STATUS_NAMES = {
@@ -201,6 +203,11 @@ class Ref(_Common):
         lib.ref_bench_prepare.restype = C.c_void_p
         lib.ref_bench_prepare.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                           C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        lib.ref_bench_prepare_i8.restype = C.c_void_p
+        lib.ref_bench_prepare_i8.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                             C.c_int, C.c_int]
+        lib.ref_bench_conv.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                       C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
         lib.ref_bench_run.argtypes = [C.c_void_p, C.c_void_p]
         lib.ref_bench_free.argtypes = [C.c_void_p]
         lib.ref_k_max.restype = C.c_longlong
@@ -209,8 +216,8 @@ class Ref(_Common):
         self.lib_pack_b = lib.ref_pack_b
 
     @staticmethod
-    def available() -> bool:
-        return os.path.exists(REF_SO)
+    def available(path: str = REF_SO) -> bool:
+        return os.path.exists(path)
 
     def _encode(self, ternary, v, rows, cols, p0, p1):
         return self.lib.ref_encode(int(ternary), _p(v), rows, cols, _p(p0), _p(p1))
@@ -265,6 +272,19 @@ class Ref(_Common):
         h = self.lib.ref_bench_prepare(mode, int(a1 is not None), _p(a0), _p(a1), m, k, int(b1 is not None),
                                        _p(b0), _p(b1), n, threads)
         return h
+
+    def bench_prepare_i8(self, mode, a, m, k, b0, b1, n, threads):
+        """"From int8 A": the timed run encodes each shard before its gemm_lowbit."""
+        return self.lib.ref_bench_prepare_i8(mode, _p(np.ascontiguousarray(a, np.int8)), m, k, int(b1 is not None),
+                                             _p(b0), _p(b1), n, threads)
+
+    def bench_conv(self, mode, fm, fm_binary, wts, w_binary, kh, kw, stride, padding, threads):
+        """`images` single-image conv2d_lowbit calls (fm: images x h x w x c) on `threads` threads."""
+        images, h, w, ch = fm.shape
+        self._chk(self.lib.ref_bench_conv(mode, _p(np.ascontiguousarray(fm, np.int8)), images, h, w, ch,
+                                          int(fm_binary), _p(np.ascontiguousarray(wts, np.int8)), wts.shape[0],
+                                          wts.shape[1], int(w_binary), kh, kw, stride, padding, threads),
+                  "bench_conv")
 
     def bench_run(self, h, c=None):
         self._chk(self.lib.ref_bench_run(h, _p(c)), "bench_run")

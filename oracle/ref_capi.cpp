@@ -179,6 +179,7 @@ struct RefBench {
     PackedB pb;
     std::vector<BinaryPackedMatrix> a_bin;
     std::vector<TernaryPackedMatrix> a_ter;
+    std::vector<SignMatrix> a_i8;  // "from int8 A": encode_* runs inside the timed call
     std::vector<int> row0;
 };
 
@@ -203,6 +204,27 @@ void* ref_bench_prepare(int mode, int a_ternary, const uint8_t* a0, const uint8_
     return rb;
 }
 
+// "From int8 A" (BASELINE.md §2 second line): the shards keep the int8 sign
+// matrix and ref_bench_run encodes each one (core.cpp:13-58) before its
+// gemm_lowbit.  pack_b stays outside, as in bench.cpp:58.
+void* ref_bench_prepare_i8(int mode, const int8_t* a, int m, int k, int b_ternary, const uint8_t* b0,
+                           const uint8_t* b1, int n, int threads) {
+    auto* rb = new RefBench;
+    rb->mode = mode;
+    rb->a_ternary = mode != 0;
+    rb->n = n;
+    rb->k = k;
+    rb->pb = packed_b_from(b_ternary, b0, b1, k, n);
+    if (threads < 1) threads = 1;
+    if (threads > m) threads = m;
+    for (int t = 0; t < threads; ++t) {
+        int r0 = (int)((long long)m * t / threads), r1 = (int)((long long)m * (t + 1) / threads);
+        rb->row0.push_back(r0);
+        rb->a_i8.push_back(sign_from(a + (size_t)r0 * k, r1 - r0, k, mode == 0));
+    }
+    return rb;
+}
+
 // Runs one full gemm over all shards; writes C (row-major m x n) if c != NULL.
 int ref_bench_run(void* h, int16_t* c) {
     auto* rb = static_cast<RefBench*>(h);
@@ -212,10 +234,18 @@ int ref_bench_run(void* h, int16_t* c) {
     for (size_t t = 0; t < shards; ++t)
         pool.emplace_back([&, t] {
             st[t] = guarded([&] {
-                int rows = rb->a_ternary ? rb->a_ter[t].rows : rb->a_bin[t].rows;
-                GemmDims dims{rows, rb->n, rb->k};
-                Int16Matrix r = rb->a_ternary ? gemm_lowbit((GemmMode)rb->mode, rb->a_ter[t], rb->pb, dims)
-                                              : gemm_lowbit((GemmMode)rb->mode, rb->a_bin[t], rb->pb, dims);
+                Int16Matrix r;
+                if (!rb->a_i8.empty()) {
+                    const SignMatrix& a = rb->a_i8[t];
+                    GemmDims dims{a.rows, rb->n, rb->k};
+                    r = rb->a_ternary ? gemm_lowbit((GemmMode)rb->mode, encode_ternary(a), rb->pb, dims)
+                                      : gemm_lowbit((GemmMode)rb->mode, encode_binary(a), rb->pb, dims);
+                } else {
+                    int rows = rb->a_ternary ? rb->a_ter[t].rows : rb->a_bin[t].rows;
+                    GemmDims dims{rows, rb->n, rb->k};
+                    r = rb->a_ternary ? gemm_lowbit((GemmMode)rb->mode, rb->a_ter[t], rb->pb, dims)
+                                      : gemm_lowbit((GemmMode)rb->mode, rb->a_bin[t], rb->pb, dims);
+                }
                 if (c) std::memcpy(c + (size_t)rb->row0[t] * rb->n, r.values.data(), r.values.size() * 2);
             });
         });
@@ -226,5 +256,34 @@ int ref_bench_run(void* h, int16_t* c) {
 }
 
 void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
+
+// Convolution baseline: `images` single-image
+// conv2d_lowbit calls (conv.cpp:33-59: im2col + encode + pack_b + gemm_lowbit,
+// all timed, as a caller of the reference pays them), images dealt to
+// `threads` std::threads.  fm: images x h x w x ch int8 (NHWC).
+int ref_bench_conv(int mode, const int8_t* fm, int images, int h, int w, int ch, int fm_binary, const int8_t* wts,
+                   int w_rows, int w_cols, int w_binary, int kh, int kw, int stride, int padding, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > images) threads = images;
+    std::vector<FeatureMap> maps;
+    for (int i = 0; i < images; ++i) {
+        FeatureMap f(h, w, ch, fm_binary ? Mode::binary : Mode::ternary);
+        std::memcpy(f.values.data(), fm + (size_t)i * h * w * ch, (size_t)h * w * ch);
+        maps.push_back(std::move(f));
+    }
+    SignMatrix wm = sign_from(wts, w_rows, w_cols, w_binary);
+    ConvSpec spec{kh, kw, stride, padding, w_cols, 1};
+    std::vector<int> st(threads, 0);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            for (int i = t; i < images && !st[t]; i += threads)
+                st[t] = guarded([&] { (void)conv2d_lowbit((GemmMode)mode, maps[i], wm, spec); });
+        });
+    for (auto& th : pool) th.join();
+    for (int x : st)
+        if (x) return x;
+    return 0;
+}
 
 }  // extern "C"

@@ -124,6 +124,7 @@ SIGNATURES = {
     "lowbit_conv2d_host": (_I, [_I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
     "lowbit_encode_host": (_I, [_I, _P, _I, _I, _P, _P, _P]),
     "lowbit_pack_b_host": (_I, [_I, _P, _P, _I, _I, _P, _P]),
+    "lowbit_release_thread_state": (None, []),
     "lowbit_generate": (_I, [_I, C.c_ulonglong, _I, _LL, _LL, _LL, _P, _P]),
 }
 

@@ -1,0 +1,154 @@
+// dropin_e2e.cpp — end to end through the C++ drop-in, exactly as a caller of
+// the reference library uses it (tests/acceptance.cpp:35-42, bench.cpp:40-68):
+// host TernaryPackedMatrix / BinaryPackedMatrix A (std::vector planes), a
+// PackedB from lowbit::pack_b, and
+//     Int16Matrix c = lowbit::gemm_lowbit(mode, a, packed_b, dims);
+// timed with the host clock around each whole call (result allocation,
+// uploads, weight preparation, GeMM, download: everything the caller waits
+// for).  Inputs come from the library's counter-based generator (identical to
+// the oracle's); the first result is checked byte-for-byte against the
+// device-resident path (lowbit_gemm on prepared weights).
+//
+//   dropin_e2e MODE M N K ITERS SEED   (MODE 0 bnn, 1 tnn, 2 tbn)
+// prints one JSON object.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../../include/lowbit_cuda.h"
+#include "lowbit/gemm.hpp"
+
+using namespace lowbit;
+
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        auto _e = (x);                                                                   \
+        if (_e) {                                                                        \
+            std::fprintf(stderr, "%s failed (%d): %s\n", #x, (int)_e, lowbit_last_error()); \
+            std::exit(2);                                                                \
+        }                                                                                \
+    } while (0)
+
+// generate + encode on the device, planes back to host vectors (reference stride)
+static void planes(int dist, unsigned long long seed, int id, int rows, int cols, bool ternary,
+                   std::vector<std::uint8_t>& p0, std::vector<std::uint8_t>& p1) {
+    int8_t* v;
+    uint8_t *d0, *d1;
+    const long long pitch = lowbit_plane_pitch(cols), sb = (cols + 7) / 8;
+    cudaMalloc(&v, (size_t)rows * cols);
+    cudaMalloc(&d0, (size_t)rows * pitch);
+    cudaMalloc(&d1, (size_t)rows * pitch);
+    int* flag;
+    cudaMalloc(&flag, 4);
+    cudaMemset(flag, 0, 4);
+    CK(lowbit_generate(dist, seed, id, 0, rows, cols, v, nullptr));
+    CK(lowbit_encode(ternary ? 1 : 0, v, rows, cols, cols, d0, ternary ? d1 : nullptr, pitch, flag, nullptr));
+    p0.resize((size_t)rows * sb);
+    cudaMemcpy2D(p0.data(), sb, d0, pitch, sb, rows, cudaMemcpyDeviceToHost);
+    if (ternary) {
+        p1.resize((size_t)rows * sb);
+        cudaMemcpy2D(p1.data(), sb, d1, pitch, sb, rows, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(v);
+    cudaFree(d0);
+    cudaFree(d1);
+    cudaFree(flag);
+}
+
+int main(int argc, char** argv) {
+    if (argc < 7) {
+        std::fprintf(stderr, "usage: dropin_e2e MODE M N K ITERS SEED\n");
+        return 1;
+    }
+    const int mode = std::atoi(argv[1]), m = std::atoi(argv[2]), n = std::atoi(argv[3]), k = std::atoi(argv[4]);
+    const int iters = std::atoi(argv[5]);
+    const unsigned long long seed = std::strtoull(argv[6], nullptr, 10);
+    const bool a_ter = mode != 0, b_ter = mode == 1;
+    const int da = mode == 0 ? 1 : (mode == 2 ? 2 : 0), db = mode == 1 ? 0 : 1;
+    TernaryPackedMatrix at;
+    BinaryPackedMatrix ab;
+    std::vector<std::uint8_t> x0, x1;
+    planes(da, seed, 0, m, k, a_ter, x0, x1);
+    if (a_ter) {
+        at.rows = m, at.cols = k, at.stride_bits = (k + 7) / 8 * 8;
+        at.plane_plus = std::move(x0);
+        at.plane_minus = std::move(x1);
+    } else {
+        ab.rows = m, ab.cols = k, ab.stride_bits = (k + 7) / 8 * 8;
+        ab.plane = std::move(x0);
+    }
+    std::vector<std::uint8_t> b0, b1;
+    planes(db, seed, 1, k, n, b_ter, b0, b1);
+    PackedB pb;
+    if (b_ter) {
+        TernaryPackedMatrix bt;
+        bt.rows = k, bt.cols = n, bt.stride_bits = (n + 7) / 8 * 8, bt.plane_plus = b0, bt.plane_minus = b1;
+        pb = pack_b(bt);
+    } else {
+        BinaryPackedMatrix bb;
+        bb.rows = k, bb.cols = n, bb.stride_bits = (n + 7) / 8 * 8, bb.plane = b0;
+        pb = pack_b(bb);
+    }
+    const GemmDims dims{m, n, k};
+    auto call = [&] {
+        return a_ter ? gemm_lowbit((GemmMode)mode, at, pb, dims) : gemm_lowbit((GemmMode)mode, ab, pb, dims);
+    };
+    // check: the drop-in result equals the device-resident path
+    Int16Matrix first = call();
+    bool equal = false;
+    {
+        const long long pitch = lowbit_plane_pitch(k), sb = (k + 7) / 8;
+        uint8_t *d0, *d1 = nullptr, *pan;
+        void* w;
+        int16_t* dc;
+        cudaMalloc(&d0, (size_t)m * pitch);
+        if (a_ter) cudaMalloc(&d1, (size_t)m * pitch);
+        cudaMemset(d0, 0, (size_t)m * pitch);
+        cudaMemcpy2D(d0, pitch, a_ter ? at.plane_plus.data() : ab.plane.data(), sb, sb, m, cudaMemcpyHostToDevice);
+        if (a_ter) {
+            cudaMemset(d1, 0, (size_t)m * pitch);
+            cudaMemcpy2D(d1, pitch, at.plane_minus.data(), sb, sb, m, cudaMemcpyHostToDevice);
+        }
+        std::vector<std::uint8_t> stream;
+        for (auto& p : pb.panels) stream.insert(stream.end(), p.buffer.begin(), p.buffer.end());
+        cudaMalloc(&pan, stream.size());
+        cudaMemcpy(pan, stream.data(), stream.size(), cudaMemcpyHostToDevice);
+        cudaMalloc(&w, lowbit_weights_bytes(b_ter, n, k));
+        CK(lowbit_prepare_weights(b_ter, pan, n, k, w, nullptr));
+        cudaMalloc(&dc, (size_t)m * n * 2);
+        CK(lowbit_gemm(mode, d0, d1, pitch, m, k, w, b_ter, n, k, m, n, k, 4096, dc, n, LOWBIT_KERNEL_AUTO, nullptr));
+        std::vector<int16_t> want((size_t)m * n);
+        cudaMemcpy(want.data(), dc, want.size() * 2, cudaMemcpyDeviceToHost);
+        equal = first.values == want;
+        cudaFree(d0);
+        if (d1) cudaFree(d1);
+        cudaFree(pan);
+        cudaFree(w);
+        cudaFree(dc);
+    }
+    first = Int16Matrix{};
+    std::vector<double> ms;
+    for (int i = 0; i < iters; ++i) {
+        auto t0 = std::chrono::steady_clock::now();
+        Int16Matrix c = call();
+        auto t1 = std::chrono::steady_clock::now();
+        ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+        if (c.values.size() != (size_t)m * n) return 3;
+    }
+    std::sort(ms.begin(), ms.end());
+    double mean = 0;
+    for (double x : ms) mean += x;
+    mean /= ms.size();
+    const double ops = 2.0 * m * n * (double)k;
+    const size_t h2d = (size_t)m * ((k + 7) / 8) * (a_ter ? 2 : 1), d2h = (size_t)m * n * 2;
+    std::printf(
+        "{\"mode\": %d, \"m\": %d, \"n\": %d, \"k\": %d, \"iters\": %d, \"ms_mean\": %.3f, \"ms_median\": %.3f, "
+        "\"TOPS\": %.3f, \"h2d_bytes_per_call\": %zu, \"d2h_bytes_per_call\": %zu, \"equal_device_path\": %s}\n",
+        mode, m, n, k, iters, mean, ms[ms.size() / 2], ops / (mean * 1e-3) / 1e12, h2d, d2h, equal ? "true" : "false");
+    return equal ? 0 : 4;
+}

@@ -2,11 +2,13 @@
 // the reference's order, kernel choice, and the host-buffer drop-in entry.
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "common.cuh"
 #include "layout.cuh"
 #include "tmap.cuh"
+#include "hostctx.cuh"
 
 namespace lb {
 lowbit_status launch_bitserial(int mode, const uint8_t* a0, const uint8_t* a1, long long a_pitch, int m, int n,
@@ -199,37 +201,37 @@ extern "C" lowbit_status lowbit_gemm_i8(int mode, const int8_t* a, long long lda
 }
 
 // ---------------------------------------------------------------------------
-// Host-buffer drop-in.  Per-thread grow-only device scratch.
+// Host-buffer drop-in.  Per-(thread, device) state, hostctx.cuh.
 // ---------------------------------------------------------------------------
 namespace {
-struct Scratch {
-    void* ptr = nullptr;
-    size_t bytes = 0;
-    cudaError_t ensure(size_t want) {
-        if (want <= bytes) return cudaSuccess;
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        bytes = 0;
-        want = (want + 0xFFFFF) & ~size_t(0xFFFFF);
-        cudaError_t e = cudaMalloc(&ptr, want);
-        if (e == cudaSuccess) bytes = want;
-        return e;
+struct ThreadState {
+    lbhost::HostCtx* ctx[lb::kMaxDevices] = {};
+    void release_all() {
+        for (auto*& c : ctx) {
+            delete c;  // ~HostCtx frees its scratch on its own device
+            c = nullptr;
+        }
     }
+    ~ThreadState() { release_all(); }
 };
-struct HostCtx {
-    static constexpr int kChunks = 8;
-    Scratch a0, a1, panels, weights, c, vals, flag;
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    cudaEvent_t ev_in[kChunks] = {}, ev_c[kChunks] = {}, ev_w = nullptr, ev_done = nullptr;
-};
-// One context per (host thread, device): scratch, streams and events belong
-// to the device that was current when they were created.
-thread_local HostCtx g_ctx[lb::kMaxDevices];
-HostCtx* host_ctx() {
-    const int dev = lb::current_device();
-    return dev < lb::kMaxDevices ? &g_ctx[dev] : nullptr;
-}
+thread_local ThreadState g_state;
 }  // namespace
+
+lbhost::HostCtx* lbhost::host_ctx() {
+    const int dev = lb::current_device();
+    if (dev < 0 || dev >= lb::kMaxDevices) return nullptr;
+    HostCtx*& c = g_state.ctx[dev];
+    if (!c) {
+        c = new HostCtx;
+        c->dev = dev;
+    }
+    return c;
+}
+
+extern "C" void lowbit_release_thread_state(void) { g_state.release_all(); }
+
+using lbhost::HostCtx;
+using lbhost::host_ctx;
 
 extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t* a1, int a_rows,
                                                  int a_cols, const uint8_t* panels, int b_ternary, int b_n, int b_k,
@@ -254,65 +256,124 @@ extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, co
     LB_CUDA_TRY(X.panels.ensure(pbytes));
     LB_CUDA_TRY(X.weights.ensure(wbytes));
     LB_CUDA_TRY(X.c.ensure((size_t)m * n * sizeof(int16_t)));
+    LB_CUDA_TRY(X.ensure_streams());
+    // Pageable caller memory (a std::vector, as the reference API hands out)
+    // goes through pinned staging slots, copied on a few host threads, so the
+    // DMA engines still run at the pinned rate; pinned memory is copied
+    // directly.
+    const bool in_pageable = !lbhost::host_pinned(a0) || (a_ternary && !lbhost::host_pinned(a1));
+    const bool out_pageable = !lbhost::host_pinned(c);
+    const bool staged = in_pageable || out_pageable;
+    const long long a_row_bytes = hstride * (a_ternary ? 2 : 1), c_row_bytes = 2LL * n;
+    int chunks;
+    long long rows_per;
+    if (staged) {  // ~16 MiB staging slots, whole 256-row m tiles
+        const long long row_bytes = a_row_bytes > c_row_bytes ? a_row_bytes : c_row_bytes;
+        rows_per = ((16LL << 20) / row_bytes) / 256 * 256;
+        if (rows_per < 256) rows_per = 256;
+        if (rows_per > m) rows_per = m;
+        chunks = (int)((m + rows_per - 1) / rows_per);
+        for (int i = 0; i < HostCtx::kBounce; ++i) {
+            if (in_pageable) LB_CUDA_TRY(X.bounce_in[i].ensure((size_t)rows_per * a_row_bytes));
+            if (out_pageable) LB_CUDA_TRY(X.bounce_out[i].ensure((size_t)rows_per * c_row_bytes));
+        }
+    } else {  // the copy-in / compute / copy-out pipeline over <= 8 chunks of >= 1024 rows
+        chunks = (int)((m + 1023) / 1024);
+        if (chunks > HostCtx::kChunks) chunks = HostCtx::kChunks;
+        if (chunks < 1) chunks = 1;
+        rows_per = (m + chunks - 1) / chunks;
+    }
+    lbhost::StreamDrain drain{{X.s_in, X.s_out, s}};  // error paths wait for queued copies
     // weights: upload + prepare once on the caller's stream
     LB_CUDA_TRY(cudaMemcpyAsync(X.panels.ptr, panels, pbytes, cudaMemcpyHostToDevice, s));
     if ((st = lowbit_prepare_weights(b_ternary, static_cast<const uint8_t*>(X.panels.ptr), n, k, X.weights.ptr,
                                      stream)))
         return st;
-    // A and C move in row chunks through a copy-in / compute / copy-out
-    // pipeline on three streams, so the PCIe directions overlap each other and
-    // the kernels (the host path is PCIe-bound: 2 B of C per output vs 1/4 B
-    // of A per input element).
-    if (!X.s_in) {
-        LB_CUDA_TRY(cudaStreamCreateWithFlags(&X.s_in, cudaStreamNonBlocking));
-        LB_CUDA_TRY(cudaStreamCreateWithFlags(&X.s_out, cudaStreamNonBlocking));
-        for (int i = 0; i < HostCtx::kChunks; ++i) {
-            LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_in[i], cudaEventDisableTiming));
-            LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_c[i], cudaEventDisableTiming));
-        }
-        LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_w, cudaEventDisableTiming));
-        LB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_done, cudaEventDisableTiming));
-    }
-    const long long min_rows = 1024;  // keep per-chunk kernels large
-    int chunks = (int)((m + min_rows - 1) / min_rows);
-    if (chunks > HostCtx::kChunks) chunks = HostCtx::kChunks;
-    if (chunks < 1) chunks = 1;
     // the copy streams must not run ahead of work already queued on `s`
     LB_CUDA_TRY(cudaEventRecord(X.ev_w, s));
     LB_CUDA_TRY(cudaStreamWaitEvent(X.s_in, X.ev_w, 0));
     LB_CUDA_TRY(cudaStreamWaitEvent(X.s_out, X.ev_w, 0));
+    lbhost::HostCopier* copier = nullptr;
+    std::unique_ptr<lbhost::HostCopier> copier_owner;
+    if (staged) {
+        copier_owner.reset(new lbhost::HostCopier(lbhost::HostCopier::default_threads()));
+        copier = copier_owner.get();
+    }
+    auto rows_of = [&](int ci, long long& r0, long long& rows) {
+        r0 = (long long)ci * rows_per;
+        rows = m - r0 < rows_per ? m - r0 : rows_per;
+    };
+    // host side of chunk `done`'s result: staging slot -> caller's C
+    auto drain_c = [&](int done, lbhost::HostCopier::Job* jobs, int& nj) -> cudaError_t {
+        long long r0, rows;
+        rows_of(done, r0, rows);
+        const int sl = done % HostCtx::kBounce;
+        cudaError_t e = cudaEventSynchronize(X.ev_bout[sl]);
+        if (e) return e;
+        jobs[nj++] = {c + r0 * n, X.bounce_out[sl].ptr, (size_t)rows * c_row_bytes};
+        return cudaSuccess;
+    };
     for (int ci = 0; ci < chunks; ++ci) {
-        const long long r0 = (long long)m * ci / chunks, r1 = (long long)m * (ci + 1) / chunks, rows = r1 - r0;
+        long long r0, rows;
+        rows_of(ci, r0, rows);
+        const int sl = ci % HostCtx::kBounce, ev = ci % HostCtx::kChunks;
         uint8_t* d0 = static_cast<uint8_t*>(X.a0.ptr) + r0 * pitch;
         uint8_t* d1 = a_ternary ? static_cast<uint8_t*>(X.a1.ptr) + r0 * pitch : nullptr;
+        const uint8_t* h0 = a0 + r0 * hstride;
+        const uint8_t* h1 = a_ternary ? a1 + r0 * hstride : nullptr;
+        if (staged) {
+            // host copies of this round: A chunk ci into its slot, and C chunk ci - kBounce
+            // (whose slot chunk ci reuses) out of it
+            lbhost::HostCopier::Job jobs[3];
+            int nj = 0;
+            if (in_pageable) {
+                if (ci >= HostCtx::kBounce) LB_CUDA_TRY(cudaEventSynchronize(X.ev_bin[sl]));  // slot's H2D done
+                uint8_t* b = static_cast<uint8_t*>(X.bounce_in[sl].ptr);
+                jobs[nj++] = {b, h0, (size_t)(rows * hstride)};
+                if (a_ternary) jobs[nj++] = {b + rows * hstride, h1, (size_t)(rows * hstride)};
+                h0 = b;
+                h1 = a_ternary ? b + rows * hstride : nullptr;
+            }
+            if (out_pageable && ci >= HostCtx::kBounce) LB_CUDA_TRY(drain_c(ci - HostCtx::kBounce, jobs, nj));
+            if (nj) copier->copy(jobs, nj);
+        }
         if (pitch == hstride) {
-            LB_CUDA_TRY(cudaMemcpyAsync(d0, a0 + r0 * hstride, rows * pitch, cudaMemcpyHostToDevice, X.s_in));
-            if (a_ternary)
-                LB_CUDA_TRY(cudaMemcpyAsync(d1, a1 + r0 * hstride, rows * pitch, cudaMemcpyHostToDevice, X.s_in));
+            LB_CUDA_TRY(cudaMemcpyAsync(d0, h0, rows * pitch, cudaMemcpyHostToDevice, X.s_in));
+            if (a_ternary) LB_CUDA_TRY(cudaMemcpyAsync(d1, h1, rows * pitch, cudaMemcpyHostToDevice, X.s_in));
         } else {  // re-pitch to 16-byte rows; zero the padding first
             LB_CUDA_TRY(cudaMemsetAsync(d0, 0, rows * pitch, X.s_in));
-            LB_CUDA_TRY(cudaMemcpy2DAsync(d0, pitch, a0 + r0 * hstride, hstride, hstride, rows,
-                                          cudaMemcpyHostToDevice, X.s_in));
+            LB_CUDA_TRY(cudaMemcpy2DAsync(d0, pitch, h0, hstride, hstride, rows, cudaMemcpyHostToDevice, X.s_in));
             if (a_ternary) {
                 LB_CUDA_TRY(cudaMemsetAsync(d1, 0, rows * pitch, X.s_in));
-                LB_CUDA_TRY(cudaMemcpy2DAsync(d1, pitch, a1 + r0 * hstride, hstride, hstride, rows,
-                                              cudaMemcpyHostToDevice, X.s_in));
+                LB_CUDA_TRY(
+                    cudaMemcpy2DAsync(d1, pitch, h1, hstride, hstride, rows, cudaMemcpyHostToDevice, X.s_in));
             }
         }
-        LB_CUDA_TRY(cudaEventRecord(X.ev_in[ci], X.s_in));
-        LB_CUDA_TRY(cudaStreamWaitEvent(s, X.ev_in[ci], 0));
+        if (in_pageable) LB_CUDA_TRY(cudaEventRecord(X.ev_bin[sl], X.s_in));
+        LB_CUDA_TRY(cudaEventRecord(X.ev_in[ev], X.s_in));
+        LB_CUDA_TRY(cudaStreamWaitEvent(s, X.ev_in[ev], 0));
         int16_t* dc = static_cast<int16_t*>(X.c.ptr) + r0 * n;
         if ((st = lowbit_gemm(mode, d0, d1, pitch, (int)rows, a_cols, X.weights.ptr, b_ternary, b_n, b_k, (int)rows,
                               n, k, k_blk, dc, n, kernel, stream)))
             return st;
-        LB_CUDA_TRY(cudaEventRecord(X.ev_c[ci], s));
-        LB_CUDA_TRY(cudaStreamWaitEvent(X.s_out, X.ev_c[ci], 0));
-        LB_CUDA_TRY(cudaMemcpyAsync(c + r0 * n, dc, (size_t)rows * n * sizeof(int16_t), cudaMemcpyDeviceToHost,
-                                    X.s_out));
+        LB_CUDA_TRY(cudaEventRecord(X.ev_c[ev], s));
+        LB_CUDA_TRY(cudaStreamWaitEvent(X.s_out, X.ev_c[ev], 0));
+        int16_t* hc = out_pageable ? static_cast<int16_t*>(X.bounce_out[sl].ptr) : c + r0 * n;
+        LB_CUDA_TRY(cudaMemcpyAsync(hc, dc, (size_t)rows * c_row_bytes, cudaMemcpyDeviceToHost, X.s_out));
+        if (out_pageable) LB_CUDA_TRY(cudaEventRecord(X.ev_bout[sl], X.s_out));
+    }
+    if (out_pageable) {  // the last kBounce results are still in their slots
+        for (int done = chunks > HostCtx::kBounce ? chunks - HostCtx::kBounce : 0; done < chunks; ++done) {
+            lbhost::HostCopier::Job jobs[1];
+            int nj = 0;
+            LB_CUDA_TRY(drain_c(done, jobs, nj));
+            copier->copy(jobs, nj);
+        }
     }
     LB_CUDA_TRY(cudaEventRecord(X.ev_done, X.s_out));
     LB_CUDA_TRY(cudaStreamWaitEvent(s, X.ev_done, 0));
     LB_CUDA_TRY(cudaStreamSynchronize(s));
+    drain.armed = false;
     return LOWBIT_OK;
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -11,6 +12,19 @@
 #define LB_DEV __device__ __forceinline__
 
 namespace lb {
+
+// Tuning / timing-experiment knobs (LOWBIT_DEBUG_FP4, LOWBIT_HALO_DEBUG, ...)
+// are read from the environment only by builds compiled with -DLOWBIT_TUNING
+// (`make TUNING=1 BUILD=... LIB=...`, loaded through LOWBIT_LIB).  The
+// product library ignores the environment: no variable can change a result.
+inline const char* tuning_env(const char* name) {
+#ifdef LOWBIT_TUNING
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 // ---------------------------------------------------------------------------
 // Bit tricks

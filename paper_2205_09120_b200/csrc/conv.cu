@@ -18,6 +18,7 @@
 #include "encode.cuh"
 #include "layout.cuh"
 #include "tmap.cuh"
+#include "hostctx.cuh"
 
 namespace lb {
 
@@ -266,7 +267,7 @@ extern "C" int lowbit_conv_select(int mode, int fm_binary, int batch, int h, int
                                   int stride, int padding, int kernel, int has_workspace) {
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
     const bool tensor = kernel == LOWBIT_KERNEL_AUTO || kernel == LOWBIT_KERNEL_TENSOR;
-    static const bool no_halo = getenv("LOWBIT_CONV_NO_HALO") != nullptr;  // tuning experiment knob
+    static const bool no_halo = lb::tuning_env("LOWBIT_CONV_NO_HALO") != nullptr;  // tuning experiment knob
     if (rows <= 0) return LOWBIT_CONV_PATH_ENCODE_GEMM;
     if (tensor && !no_halo && lb::conv_halo_applies(fm_binary, h, w, c, cout, kh, kw, stride, padding, batch))
         return LOWBIT_CONV_PATH_HALO_FP4;
@@ -321,27 +322,6 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
                        cout, kernel, stream);
 }
 
-namespace {
-struct ConvScratch {
-    void* ptr = nullptr;
-    size_t bytes = 0;
-    cudaError_t ensure(size_t want) {
-        if (want <= bytes) return cudaSuccess;
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        bytes = 0;
-        want = (want + 0xFFFFF) & ~size_t(0xFFFFF);
-        cudaError_t e = cudaMalloc(&ptr, want);
-        if (e == cudaSuccess) bytes = want;
-        return e;
-    }
-};
-struct ConvHostCtx {
-    ConvScratch fm, ws, pan, w, out, out32, flag;
-};
-thread_local ConvHostCtx g_conv_ctx[kMaxDevices];  // per (host thread, device)
-}  // namespace
-
 extern "C" lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
                                             const uint8_t* panels, int b_ternary, int cout, int k, int kh, int kw,
                                             int stride, int padding, int binary_pad_value, int32_t* out,
@@ -354,11 +334,11 @@ extern "C" lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batc
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
     const size_t fm_bytes = (size_t)batch * h * w * c;
     const size_t pbytes = lowbit_packed_b_bytes(b_ternary, cout, k);
-    const int dev = current_device();
-    if (dev >= kMaxDevices) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d_host: device ordinal out of range");
-    ConvHostCtx& X = g_conv_ctx[dev];
-    ConvScratch &g_fm = X.fm, &g_ws = X.ws, &g_pan = X.pan, &g_w = X.w, &g_out = X.out, &g_out32 = X.out32,
-                &g_flag = X.flag;
+    lbhost::HostCtx* Xp = lbhost::host_ctx();
+    if (!Xp) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv2d_host: device ordinal out of range");
+    lbhost::HostCtx& X = *Xp;
+    lbhost::DevScratch &g_fm = X.fm, &g_ws = X.ws, &g_pan = X.panels, &g_w = X.weights, &g_out = X.out16,
+                       &g_out32 = X.out32, &g_flag = X.flag;
     LB_CUDA_TRY(g_fm.ensure(fm_bytes + 16));
     LB_CUDA_TRY(g_ws.ensure(lowbit_conv2d_workspace_bytes(mode, batch, h, w, c, kh, kw, stride, padding)));
     LB_CUDA_TRY(g_pan.ensure(pbytes));

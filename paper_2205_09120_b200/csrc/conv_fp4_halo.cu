@@ -524,15 +524,15 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
     if (g.kblocks > H7_MAX_KB || cb * g.raw_cb > H7_RAW_MAX) return g;
     // 16 epilogue warps when their staging fits, else 8; ring depths: fp4 3 (2 if tight),
     // raw whatever is left (<= 4, >= 2)
-    static const int f4_max = getenv("LOWBIT_HALO_F4ST") ? atoi(getenv("LOWBIT_HALO_F4ST")) : 3;  // tuning knob
-    static const int nepi_max = getenv("LOWBIT_HALO_NEPI8") ? 8 : 16;                            // tuning knob
+    static const int f4_max = lb::tuning_env("LOWBIT_HALO_F4ST") ? atoi(lb::tuning_env("LOWBIT_HALO_F4ST")) : 3;  // tuning knob
+    static const int nepi_max = lb::tuning_env("LOWBIT_HALO_NEPI8") ? 8 : 16;                            // tuning knob
     for (int nepi = nepi_max; nepi >= 8; nepi -= 8) {
         const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - h7_epi_bytes(nepi) - g.kblocks * g.breg;
         for (int f4 = f4_max; f4 >= 2; --f4) {
             const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
             if (raw >= 2) {
                 g.f4_st = f4;
-                static const int raw_max = getenv("LOWBIT_HALO_RAWST") ? atoi(getenv("LOWBIT_HALO_RAWST")) : H7_MAX_ST;
+                static const int raw_max = lb::tuning_env("LOWBIT_HALO_RAWST") ? atoi(lb::tuning_env("LOWBIT_HALO_RAWST")) : H7_MAX_ST;
                 g.raw_st = raw < raw_max ? raw : raw_max;  // (tuning knob: LOWBIT_HALO_RAWST caps the raw ring)
                 g.nepi = nepi;
                 g.ok = true;
@@ -595,7 +595,7 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     prm.acc_cols = prm.nacc == 3 ? (int)H7_SF_COL / 3 : H7_MAX_BN;
     prm.k33 = kh == 3 && kw == 3 && prm.cblocks == 1;
     prm.check_zero = check_zero;
-    static const int dbg = getenv("LOWBIT_HALO_DEBUG") ? atoi(getenv("LOWBIT_HALO_DEBUG")) : 0;
+    static const int dbg = lb::tuning_env("LOWBIT_HALO_DEBUG") ? atoi(lb::tuning_env("LOWBIT_HALO_DEBUG")) : 0;
     prm.dbg = dbg;
     prm.out = out;
     prm.zero_flag = zero_flag;
@@ -618,7 +618,7 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     cfg.dynamicSmemBytes = H7_SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
-    static const bool no_pdl = getenv("LOWBIT_NO_PDL") != nullptr;  // tuning experiment knob
+    static const bool no_pdl = lb::tuning_env("LOWBIT_NO_PDL") != nullptr;  // tuning experiment knob
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
     cfg.attrs = at;

@@ -579,18 +579,18 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
     const int oh = (h + 2 * pad - kh) / stride + 1, ow = (w + 2 * pad - kw) / stride + 1;
     const long long rows = (long long)batch * oh * ow;
     const int k = kh * kw * cch;
-    static const bool no_tl = getenv("LOWBIT_CONV_IM2COL") != nullptr;  // tuning experiment knob
+    static const bool no_tl = lb::tuning_env("LOWBIT_CONV_IM2COL") != nullptr;  // tuning experiment knob
     const bool tl = halo_ok(batch, h, w, cch, cout, kh, kw, stride, pad) && !no_tl;
     const int hp = h + 2 * pad, wp = halo_pitch(w, pad);
     uint8_t* fm4 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 1023) & ~uintptr_t(1023));
-    static bool carve[kMaxDevices] = {};
+    static std::atomic<bool> carve[kMaxDevices] = {};  // idempotent attribute: racing setters agree
     const int cdev = current_device();
-    if (cdev >= kMaxDevices || !carve[cdev]) {  // run the pack passes with K6's shared-memory carveout: no L1/smem reconfiguration between them
+    if (cdev >= kMaxDevices || !carve[cdev].load(std::memory_order_relaxed)) {  // run the pack passes with K6's shared-memory carveout: no L1/smem reconfiguration between them
         cudaFuncSetAttribute(conv_pack_fp4_padded_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(conv_pack_fp4_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        if (cdev < kMaxDevices) carve[cdev] = true;
+        if (cdev < kMaxDevices) carve[cdev].store(true, std::memory_order_relaxed);
     }
     if (tl) {
         const int prows = batch * hp;
@@ -626,11 +626,11 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
     prm.hpwp = hp * wp;
     prm.hloads = halo_loads(w, pad, kh, kw);
     prm.oh_kh = kh;
-    static const int epi_split = getenv("LOWBIT_CONV_EPI_ALT") ? 0 : 1;  // tuning experiment knob
+    static const int epi_split = lb::tuning_env("LOWBIT_CONV_EPI_ALT") ? 0 : 1;  // tuning experiment knob
     prm.epi_split = epi_split;
     prm.nacc = 3 * prm.bn <= (int)C6_SF_COL ? 3 : 2;
     prm.acc_cols = prm.nacc == 3 ? (int)C6_SF_COL / 3 : C6_MAX_BN;
-    static const int dbg = getenv("LOWBIT_CONV_DEBUG") ? atoi(getenv("LOWBIT_CONV_DEBUG")) : 0;
+    static const int dbg = lb::tuning_env("LOWBIT_CONV_DEBUG") ? atoi(lb::tuning_env("LOWBIT_CONV_DEBUG")) : 0;
     prm.dbg = dbg;
     prm.breg = ((prm.bn / 2) * 64 + 1023) / 1024 * 1024;
     prm.a_st = (C6_RING_BUDGET - prm.kblocks * prm.breg) /

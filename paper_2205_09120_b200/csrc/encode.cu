@@ -195,11 +195,12 @@ __global__ void prepare_i8_kernel(int ternary, const uint8_t* __restrict__ panel
     }
 }
 
-// fp4 (e2m1) section: one thread per (column, 16-byte chunk = 32 depth
-// positions); +1 -> 0x2, -1 -> 0xA, 0 -> 0x0, element 2i in the low nibble
-// of byte i; zero past k.
+// fp4 (e2m1) sections: one thread per (column, 16-byte chunk = 32 depth
+// positions); +1 -> 0x2, -1 -> 0xA, 0 -> 0x0, zero past k.
+//   out  (canonical): element 2i in the low nibble of byte i.
+//   outr (reference order, layout.cuh): nibble 8q+i holds element 4i+q.
 __global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ panels, int n, int k, int np, int kp4,
-                                   uint8_t* __restrict__ out) {
+                                   uint8_t* __restrict__ out, uint8_t* __restrict__ outr) {
     const int db = (k + 7) / 8;
     const int chunks = kp4 / 32;
     const long long total = (long long)np * chunks;
@@ -207,8 +208,9 @@ __global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ pane
          idx += (long long)gridDim.x * blockDim.x) {
         const int col = (int)(idx / chunks);
         const int ch = (int)(idx - (long long)col * chunks);
-        uint32_t words[4] = {0, 0, 0, 0};
+        uint32_t words[4] = {0, 0, 0, 0}, rwords[4] = {0, 0, 0, 0};
         if (col < n) {
+            uint32_t pw = 0, mw = 0;  // the chunk's 32 plus / minus bits, element e at bit e
 #pragma unroll
             for (int q = 0; q < 4; ++q) {  // 8 depth positions (one panel byte) per output word
                 const int d = ch * 4 + q;
@@ -222,16 +224,25 @@ __global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ pane
                     const int valid = k - d * 8 < 8 ? k - d * 8 : 8;
                     p = ~m & ((1u << valid) - 1u);
                 }
-                uint32_t w = 0;
+                pw |= p << (8 * q);
+                mw |= m << (8 * q);
+            }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t code = ((p >> j) & 1u) ? 0x2u : (((m >> j) & 1u) ? 0xAu : 0x0u);
-                    w |= code << (4 * j);
+            for (int q = 0; q < 4; ++q) {
+                uint32_t w = 0, wr = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int e = 8 * q + i, er = 4 * i + q;
+                    w |= (((pw >> e) & 1u) ? 0x2u : (((mw >> e) & 1u) ? 0xAu : 0x0u)) << (4 * i);
+                    wr |= (((pw >> er) & 1u) ? 0x2u : (((mw >> er) & 1u) ? 0xAu : 0x0u)) << (4 * i);
                 }
                 words[q] = w;
+                rwords[q] = wr;
             }
         }
         reinterpret_cast<uint4*>(out + (size_t)col * (kp4 / 2))[ch] = make_uint4(words[0], words[1], words[2], words[3]);
+        reinterpret_cast<uint4*>(outr + (size_t)col * (kp4 / 2))[ch] =
+            make_uint4(rwords[0], rwords[1], rwords[2], rwords[3]);
     }
 }
 
@@ -333,7 +344,7 @@ extern "C" lowbit_status lowbit_prepare_weights(int ternary, const uint8_t* pane
         ternary, panels, n, k, L.np, L.kp, reinterpret_cast<int8_t*>(base));
     LB_CUDA_TRY(cudaGetLastError());
     prepare_fp4_kernel<<<grid_for((long long)L.np * (L.kp4 / 32), 256), 256, 0, s>>>(
-        ternary, panels, n, k, L.np, L.kp4, base + L.off_fp4);
+        ternary, panels, n, k, L.np, L.kp4, base + L.off_fp4, base + L.off_fp4r);
     LB_CUDA_TRY(cudaGetLastError());
     prepare_bits_kernel<<<grid_for((long long)L.np * L.kw, 256), 256, 0, s>>>(
         ternary, panels, n, k, L.np, L.kw, reinterpret_cast<uint32_t*>(base + L.off_sign),

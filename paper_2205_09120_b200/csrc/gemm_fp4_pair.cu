@@ -127,27 +127,17 @@ __device__ unsigned long long g_fp4_stats[16];
 #define F4_ACC(var) \
     if (prm.debug & 8) var += clock64() - _t0
 
-// One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1.
-// Reference bit order (element j of a word at bit j): byte q of the word ->
-// its 8 bits one per nibble (bit k -> bit 4k).
-__device__ __forceinline__ uint32_t spread8_nibbles(uint32_t b) {
-    uint32_t x = (b | (b << 12)) & 0x000F000Fu;
-    x = (x | (x << 6)) & 0x03030303u;
-    return (x | (x << 3)) & 0x11111111u;
-}
-
-// LAYOUT 2 (NIBBLES): ~4.5 integer ops per 8 elements; LAYOUT 0 (REFERENCE
-// planes, the reference's own encoding): ~16 ternary / ~9 binary.
-template <bool A_TER, int LAYOUT>
+// One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1:
+// output word q takes bit 4i+q of the plane word into nibble i — one shift +
+// mask per plane and an IMAD, ~4.5 integer ops per 8 elements.  For NIBBLES
+// planes (element j at bit 4*(j%8) + j/8) that is element 8q+i, the canonical
+// order of the fp4 B section; for REFERENCE planes (element j at bit j) it is
+// element 4i+q, the order of the reference-order B section (layout.cuh), so
+// both layouts cost the same here.
+template <bool A_TER>
 __device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) {
     uint32_t o[4];
-    if (LAYOUT == 0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t ps = spread8_nibbles((p >> (8 * q)) & 0xFFu);
-            o[q] = A_TER ? spread8_nibbles((m >> (8 * q)) & 0xFFu) * 10u + (ps << 1) : ps * 8u + 0x22222222u;
-        }
-    } else if (A_TER) {
+    if (A_TER) {
         o[0] = (m & 0x11111111u) * 10u + ((p << 1) & 0x22222222u);
         o[1] = ((m >> 1) & 0x11111111u) * 10u + (p & 0x22222222u);
         o[2] = ((m >> 2) & 0x11111111u) * 10u + ((p >> 1) & 0x22222222u);
@@ -163,7 +153,7 @@ __device__ __forceinline__ void fp4_chunk(uint32_t p, uint32_t m, uint32_t dst) 
 // n tiles in lockstep and share B: each CTA loads one k-block half of a B stage
 // and multicasts it to the same-position CTA of the other pair, halving B's
 // L2 -> SM traffic.
-template <bool A_TER, bool AR, int LAYOUT, int CL>
+template <bool A_TER, bool AR, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
     gemm_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a0,
                          const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_c,
@@ -522,14 +512,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 F4_T0();
                 const uint32_t row = sA_u + kb * F4_A_BYTES + r * 128;
                 const uint32_t sw = (uint32_t)r & 7;  // SW128: chunk c at c ^ (row % 8)
-                fp4_chunk<A_TER, LAYOUT>(p0.x, m0.x, row + ((0 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p0.y, m0.y, row + ((1 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p0.z, m0.z, row + ((2 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p0.w, m0.w, row + ((3 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p1.x, m1.x, row + ((4 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p1.y, m1.y, row + ((5 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p1.z, m1.z, row + ((6 ^ sw) << 4));
-                fp4_chunk<A_TER, LAYOUT>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.x, m0.x, row + ((0 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.y, m0.y, row + ((1 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.z, m0.z, row + ((2 ^ sw) << 4));
+                fp4_chunk<A_TER>(p0.w, m0.w, row + ((3 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.x, m1.x, row + ((4 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
+                fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(a_ready0 + (kb >> 1) * 8);
@@ -567,14 +557,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             }
             const uint32_t row = sA_u + st * F4_A_BYTES + r * 128;
             const uint32_t sw = (uint32_t)r & 7;  // SW128: chunk c at c ^ (row % 8)
-            fp4_chunk<A_TER, LAYOUT>(p0.x, m0.x, row + ((0 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p0.y, m0.y, row + ((1 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p0.z, m0.z, row + ((2 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p0.w, m0.w, row + ((3 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p1.x, m1.x, row + ((4 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p1.y, m1.y, row + ((5 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p1.z, m1.z, row + ((6 ^ sw) << 4));
-            fp4_chunk<A_TER, LAYOUT>(p1.w, m1.w, row + ((7 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.x, m0.x, row + ((0 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.y, m0.y, row + ((1 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.z, m0.z, row + ((2 ^ sw) << 4));
+            fp4_chunk<A_TER>(p0.w, m0.w, row + ((3 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.x, m1.x, row + ((4 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.y, m1.y, row + ((5 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.z, m1.z, row + ((6 ^ sw) << 4));
+            fp4_chunk<A_TER>(p1.w, m1.w, row + ((7 ^ sw) << 4));
             }
         done:
             fence_proxy_async_smem();
@@ -769,15 +759,15 @@ static int pick_bn_fp4(int n, int max_bn = F4_MAX_BN) {
     return (per + 31) / 32 * 32;
 }
 
-template <bool A_TER, bool AR, int LAYOUT, int CL = 2>
+template <bool A_TER, bool AR, int CL = 2>
 static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap& ma0, const CUtensorMap& ma1,
                                         const CUtensorMap& mc, const Fp4Params& prm, int pairs, cudaStream_t stream) {
     static SmemOptIn attr;
-    static int max_clusters = 0;
+    int max_clusters = 0;  // CL = 4 experiment only: queried per launch (per device)
     constexpr int smem = f4_smem_bytes(AR);
-    auto kern = gemm_fp4_pair_kernel<A_TER, AR, LAYOUT, CL>;
+    auto kern = gemm_fp4_pair_kernel<A_TER, AR, CL>;
     LB_CUDA_TRY(attr.ensure(kern, smem));
-    if (CL == 4 && !max_clusters) {
+    if (CL == 4) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(4 * 37);
         cfg.blockDim = dim3(F4_THREADS);
@@ -790,10 +780,10 @@ static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap
         if (max_clusters > 0 && clusters > max_clusters) clusters = max_clusters;
         grid = 4 * (clusters > 0 ? clusters : 1);
     }
-    static const bool verbose = getenv("LOWBIT_FP4_VERBOSE") != nullptr;
+    static const bool verbose = tuning_env("LOWBIT_FP4_VERBOSE") != nullptr;
     if (verbose)
-        std::fprintf(stderr, "fp4 kernel: AR %d layout %d CL %d grid %d (max clusters %d) bn %d n_tiles %d m_tiles %d\n",
-                     (int)AR, LAYOUT, CL, grid, max_clusters, prm.bn, prm.n_tiles, prm.m_tiles);
+        std::fprintf(stderr, "fp4 kernel: AR %d CL %d grid %d (max clusters %d) bn %d n_tiles %d m_tiles %d\n",
+                     (int)AR, CL, grid, max_clusters, prm.bn, prm.n_tiles, prm.m_tiles);
     kern<<<grid, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
@@ -815,7 +805,7 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
     prm.c = c;
     prm.tma_store = ((ldc * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
     static const bool direct_epi = [] {
-        const char* e = getenv("LOWBIT_FP4_EPI");
+        const char* e = tuning_env("LOWBIT_FP4_EPI");
         return e && e[0] == 'd';
     }();
     if (direct_epi) prm.tma_store = 0;
@@ -826,7 +816,7 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
     prm.resident = prm.m_major && prm.kblocks <= f4_raw_stages(a_ternary != 0) &&
                    (prm.kblocks % 2 == 0 || prm.n_tiles == 1);
     static const int no_ar = [] {
-        const char* e = getenv("LOWBIT_FP4_NO_AR");  // tuning experiments: force the streaming variant
+        const char* e = tuning_env("LOWBIT_FP4_NO_AR");  // tuning experiments: force the streaming variant
         return e ? atoi(e) : 0;
     }();
     prm.a_res = !no_ar && prm.m_major && prm.n_tiles >= 2 && prm.kblocks <= F4_AR_SLOTS && prm.kblocks % 2 == 0;
@@ -836,12 +826,15 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
         prm.n_tiles = (n + prm.bn - 1) / prm.bn;
     }
     static const int debug = [] {
-        const char* e = getenv("LOWBIT_DEBUG_FP4");
+        const char* e = tuning_env("LOWBIT_DEBUG_FP4");
         return e ? atoi(e) : 0;
     }();
     prm.debug = debug;
     CUtensorMap mb, ma0, ma1, mc;
-    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
+    // NIBBLES planes pair with the canonical fp4 B section, REFERENCE planes with
+    // the reference-order one (layout.cuh): the converters are the same
+    const uint8_t* wfp4 =
+        static_cast<const uint8_t*>(weights) + (layout == LOWBIT_LAYOUT_NIBBLES ? L.off_fp4 : L.off_fp4r);
     if (!make_map_2d(&mb, wfp4, (uint64_t)L.kp4 / 2, (uint64_t)L.np, (uint64_t)L.kp4 / 2, 128, (uint32_t)(prm.bn / 2),
                      CU_TENSOR_MAP_SWIZZLE_128B))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for fp4 B");
@@ -864,28 +857,20 @@ lowbit_status launch_fp4_pair(int a_ternary, int layout, const uint8_t* a0, cons
     }
     const int work = prm.m_major ? prm.m_tiles : prm.m_tiles * prm.n_tiles;
     const int pairs = work < num_sms() / 2 ? work : num_sms() / 2;
-#define F4_LAUNCH(TER, AR_, LAY) launch_fp4_variant<TER, AR_, LAY>(mb, ma0, ma1, mc, prm, pairs, stream)
+#define F4_LAUNCH(TER, AR_) launch_fp4_variant<TER, AR_>(mb, ma0, ma1, mc, prm, pairs, stream)
     static const int cl4 = [] {
-        const char* e = getenv("LOWBIT_FP4_CL4");  // 4-CTA clusters with multicast B for the AR variant
+        const char* e = tuning_env("LOWBIT_FP4_CL4");  // 4-CTA clusters with multicast B for the AR variant
         return e ? atoi(e) : 0;
     }();
     if (prm.a_res && cl4) {
-        // Tuning experiment (LOWBIT_FP4_CL4=1): multicast B across 4-CTA clusters.  Per SM the
-        // k-block time drops ~8% (half the B traffic), but only 33 clusters (132 SMs) fit the
-        // GPCs, so it measured 3% slower on c5 (and ~0.5% faster when the leftover TPCs ran a
-        // concurrent pair kernel on the remaining m tiles).
-        return layout == LOWBIT_LAYOUT_NIBBLES
-                   ? (a_ternary ? launch_fp4_variant<true, true, 2, 4>(mb, ma0, ma1, mc, prm, pairs, stream)
-                                : launch_fp4_variant<false, true, 2, 4>(mb, ma0, ma1, mc, prm, pairs, stream))
-                   : (a_ternary ? launch_fp4_variant<true, true, 0, 4>(mb, ma0, ma1, mc, prm, pairs, stream)
-                                : launch_fp4_variant<false, true, 0, 4>(mb, ma0, ma1, mc, prm, pairs, stream));
+        // Tuning experiment (LOWBIT_FP4_CL4=1, LOWBIT_TUNING builds): multicast B across 4-CTA
+        // clusters.  Per SM the k-block time drops ~8% (half the B traffic), but only 33 clusters
+        // (132 SMs) fit the GPCs, so it measured 3% slower on c5.
+        return a_ternary ? launch_fp4_variant<true, true, 4>(mb, ma0, ma1, mc, prm, pairs, stream)
+                         : launch_fp4_variant<false, true, 4>(mb, ma0, ma1, mc, prm, pairs, stream);
     }
-    if (layout == LOWBIT_LAYOUT_NIBBLES) {
-        if (prm.a_res) return a_ternary ? F4_LAUNCH(true, true, 2) : F4_LAUNCH(false, true, 2);
-        return a_ternary ? F4_LAUNCH(true, false, 2) : F4_LAUNCH(false, false, 2);
-    }
-    if (prm.a_res) return a_ternary ? F4_LAUNCH(true, true, 0) : F4_LAUNCH(false, true, 0);
-    return a_ternary ? F4_LAUNCH(true, false, 0) : F4_LAUNCH(false, false, 0);
+    if (prm.a_res) return a_ternary ? F4_LAUNCH(true, true) : F4_LAUNCH(false, true);
+    return a_ternary ? F4_LAUNCH(true, false) : F4_LAUNCH(false, false);
 #undef F4_LAUNCH
 }
 

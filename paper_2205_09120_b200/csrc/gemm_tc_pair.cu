@@ -431,7 +431,7 @@ static PairParams pair_params(int m, int n, int k, int b_ternary, int16_t* c, lo
     prm.c = c;
     prm.tma_store = ((ldc * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
     static const int debug = [] {
-        const char* e = getenv("LOWBIT_DEBUG_PAIR");
+        const char* e = lb::tuning_env("LOWBIT_DEBUG_PAIR");
         return e ? atoi(e) : 0;
     }();
     prm.debug = debug;

@@ -12,6 +12,16 @@
 //                     -1 = 0xA, 0 = 0x0; element 2i in the low nibble of
 //                     byte i), kp4 a multiple of 256: the UMMA B operand of
 //                     the kind::mxf4 path.
+//   [ fp4 section, reference order ]
+//                     the same codes with the 32 depth positions of every
+//                     16-byte chunk permuted: byte-nibble position 8q+i holds
+//                     depth element 4i+q of the chunk.  That is the order in
+//                     which ((w >> q) & 0x11111111) lays a plane word of the
+//                     REFERENCE bit order (element j at bit j, core.hpp:3-10)
+//                     into nibbles, so K5 turns reference planes into its A
+//                     operand with the same one shift + mask per plane as the
+//                     NIBBLES layout, and the MMA's depth sum is unchanged
+//                     (A and B are permuted alike; padding is 0 in both).
 #pragma once
 #include <cstddef>
 
@@ -23,7 +33,7 @@ struct WeightsLayout {
     int kp;  // int8 row length, multiple of 128 bytes (one UMMA k-block)
     int kw;  // words per column in the bit sections, multiple of 8 (one K2 stage)
     int kp4; // fp4 row length in elements, multiple of 256 (one 128-byte fp4 k-block)
-    size_t off_sign, off_nz, off_fp4, bytes;
+    size_t off_sign, off_nz, off_fp4, off_fp4r, bytes;
 
     __host__ __device__ WeightsLayout(int ternary_, int n_, int k_) : ternary(ternary_), n(n_), k(k_) {
         np = (n + 255) / 256 * 256;
@@ -33,7 +43,8 @@ struct WeightsLayout {
         off_sign = (size_t)np * kp;
         off_nz = off_sign + (size_t)np * kw * 4;
         off_fp4 = (off_nz + (ternary ? (size_t)np * kw * 4 : 0) + 1023) / 1024 * 1024;
-        bytes = off_fp4 + (size_t)np * kp4 / 2;
+        off_fp4r = off_fp4 + (size_t)np * kp4 / 2;
+        bytes = off_fp4r + (size_t)np * kp4 / 2;
     }
 };
 

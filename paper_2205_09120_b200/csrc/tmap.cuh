@@ -3,6 +3,9 @@
 #pragma once
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace lb {
@@ -109,32 +112,36 @@ constexpr int kMaxDevices = 64;
 // SM count of the current device (cached per device: one process may drive
 // several GPUs from different host threads).
 inline int num_sms() {
-    static int sms[kMaxDevices] = {};
+    static std::atomic<int> sms[kMaxDevices] = {};  // 0 = not queried yet; racing writers store the same value
     const int dev = current_device();
-    if (dev >= kMaxDevices) {
+    int v = dev < kMaxDevices ? sms[dev].load(std::memory_order_relaxed) : 0;
+    if (!v) {
         int n = 0;
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n > 0 ? n : 148;
+        v = n > 0 ? n : 148;
+        if (dev < kMaxDevices) sms[dev].store(v, std::memory_order_relaxed);
     }
-    if (!sms[dev]) {
-        int n = 0;
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        sms[dev] = n > 0 ? n : 148;
-    }
-    return sms[dev];
+    return v;
 }
 
 // Largest dynamic-shared-memory opt-in already applied to one kernel, per
-// device (cudaFuncSetAttribute is per device).  ensure() sets the attribute
-// the first time a device needs `bytes` or more.
+// device (cudaFuncSetAttribute is per device).  ensure() raises the
+// attribute the first time a device needs more than it holds.  The opt-in
+// only ever grows and the attribute call and the cache update happen under
+// one lock, so concurrent host threads asking for different sizes cannot
+// leave the cache above what the driver holds.
 struct SmemOptIn {
-    int bytes[kMaxDevices] = {};
+    std::atomic<int> bytes[kMaxDevices] = {};
+    std::mutex mu;
     template <typename K>
     cudaError_t ensure(K kern, int need) {
         const int dev = current_device();
-        if (dev < kMaxDevices && bytes[dev] >= need) return cudaSuccess;
+        if (dev < kMaxDevices && bytes[dev].load(std::memory_order_acquire) >= need) return cudaSuccess;
+        std::lock_guard<std::mutex> lock(mu);
+        const int have = dev < kMaxDevices ? bytes[dev].load(std::memory_order_relaxed) : 0;
+        if (have >= need) return cudaSuccess;
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
-        if (e == cudaSuccess && dev < kMaxDevices) bytes[dev] = need;
+        if (e == cudaSuccess && dev < kMaxDevices) bytes[dev].store(need, std::memory_order_release);
         return e;
     }
 };
