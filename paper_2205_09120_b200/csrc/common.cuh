@@ -38,6 +38,23 @@ LB_DEV uint32_t gather_msb4(uint32_t x) { return (((x >> 7) & 0x01010101u) * 0x0
 // Per-byte "is nonzero" flag in bit 7 of each byte.
 LB_DEV uint32_t nonzero_msb(uint32_t x) { return ((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu | x) & 0x80808080u; }
 
+// Per-byte sign of 4 int8 values: 0x01 (v > 0), 0xFF (v < 0), 0x00 — the
+// value encode_ternary sees (core.cpp:40-58).  PRMT's sign-replicate
+// selectors (0x8-0xB) give 0xFF per negative byte; OR the nonzero flag.
+LB_DEV uint32_t sign_mask_i8x4(uint32_t x) {  // 0xFF per negative byte, else 0x00
+    uint32_t m;
+    asm("prmt.b32 %0, %1, %2, 0xBA98;" : "=r"(m) : "r"(x), "r"(0u));
+    return m;
+}
+LB_DEV uint32_t sign_i8x4(uint32_t x) { return sign_mask_i8x4(x) | (nonzero_msb(x) >> 7); }
+// Nonzero iff some byte of x is outside {-1, 0, +1} (two ops: PRMT + LOP3).  With
+// m the sign mask, (x ^ m) is 0x00 for 0x00 / 0xFF and 0x01 for 0x01 (kept by the
+// 0xFE mask only when m = 0) — anything else leaves a bit set.
+LB_DEV uint32_t out_of_sign_domain(uint32_t x) {
+    const uint32_t m = sign_mask_i8x4(x);
+    return (x ^ m) & (m | 0xFEFEFEFEu);
+}
+
 // 4-bit nibble -> 0x01 in byte j for each set bit j (no carries: partial
 // products land on 16 distinct bit positions).
 LB_DEV uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
@@ -309,6 +326,15 @@ LB_DEV void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, uint32_t m
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_leader_form), "r"(x), "r"(y), "h"(cta_mask)
+        : "memory");
+}
+// im2col-mode TMA into this CTA's shared memory, completion on a local barrier.
+LB_DEV void tma_load_im2col_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c, int w, int h, int n,
+                               uint16_t off_w, uint16_t off_h) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.im2col.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
         : "memory");
 }
 // im2col-mode TMA (pair form): 4-D NHWC map {c, w, h, n} + filter-tap offsets.

@@ -30,8 +30,9 @@
 //     swizzled staging box and TMA-stores 32 pixels x 64 columns, clipped at
 //     the image edges by the tensor map.
 //   * Encoding: +-1 activations become +-0.5 (e2m1 0x1 / 0x9 = the int8 byte
-//     AND 0x09), the filter stays +-1.0, and the epilogue doubles the exact
-//     half-integer sums.
+//     AND 0x09; a chunk holding any value outside {-1, 0, +1} is mapped by
+//     sign, as encode_ternary does), the filter stays +-1.0, and the epilogue
+//     doubles the exact half-integer sums.
 //
 // Warp roles per CTA (NEPI = 16: 864 threads, or 8: 608): 0 .. NEPI-1
 // epilogue (two warps per TMEM lane quarter and tile, each half of the tile's
@@ -117,6 +118,19 @@ LB_DEV uint32_t h7_pack8(uint32_t x0, uint32_t x1) {
     const uint32_t c0 = x0 & 0x09090909u, c1 = x1 & 0x09090909u;
     const uint32_t t0 = c0 | (c0 >> 4), t1 = c1 | (c1 >> 4);  // byte 0 = ch0 | ch1 << 4, byte 2 = ch2 | ch3 << 4
     return __byte_perm(t0, t1, 0x6420);
+}
+// Any int8 value, by SIGN as encode_ternary maps it (core.cpp:40-58: v > 0 -> +1,
+// v < 0 -> -1): the code is the nonzero flag in bit 0 and the sign bit in bit 3.
+// The converters take this path only for a 16-channel chunk that holds a value
+// outside {-1, 0, +1} (out_of_sign_domain: two ops per word on the fast path).
+LB_DEV uint32_t h7_code4(uint32_t x) { return (nonzero_msb(x) >> 7) | ((x >> 4) & 0x08080808u); }
+LB_DEV uint32_t h7_pack8_sign(uint32_t x0, uint32_t x1) {
+    const uint32_t c0 = h7_code4(x0), c1 = h7_code4(x1);
+    const uint32_t t0 = c0 | (c0 >> 4), t1 = c1 | (c1 >> 4);
+    return __byte_perm(t0, t1, 0x6420);
+}
+LB_DEV uint32_t h7_bad16(uint4 v) {
+    return out_of_sign_domain(v.x) | out_of_sign_domain(v.y) | out_of_sign_domain(v.z) | out_of_sign_domain(v.w);
 }
 // all 16 bytes nonzero (a binary map holds no 0, core.cpp:23)
 LB_DEV bool h7_all_nonzero(uint4 v) {
@@ -273,15 +287,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                             uint4 v[8];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) v[q] = lds_v4(src + raw_off(jb + STEP * q));
+                            uint32_t bad = 0;
 #pragma unroll
-                            for (int q = 0; q < 8; ++q)
+                            for (int q = 0; q < 8; ++q) {
                                 sts_v2(dst + (uint32_t)(jb + STEP * q) * 64u, h7_pack8(v[q].x, v[q].y),
                                        h7_pack8(v[q].z, v[q].w));
+                                bad |= h7_bad16(v[q]);
+                            }
+                            if (bad != 0) {  // a value outside {-1, 0, +1}: rewrite the chunks by sign
+#pragma unroll
+                                for (int q = 0; q < 8; ++q)
+                                    sts_v2(dst + (uint32_t)(jb + STEP * q) * 64u, h7_pack8_sign(v[q].x, v[q].y),
+                                           h7_pack8_sign(v[q].z, v[q].w));
+                            }
                         }
                         for (int q = 0; q < nrem; ++q) {
                             const int j = j0 + nfull * 8 * STEP + STEP * q;
                             const uint4 v = lds_v4(src + raw_off(j));
-                            sts_v2(dst + (uint32_t)j * 64u, h7_pack8(v.x, v.y), h7_pack8(v.z, v.w));
+                            sts_v2(dst + (uint32_t)j * 64u, h7_pack8_sign(v.x, v.y), h7_pack8_sign(v.z, v.w));
                         }
                     }
                 if (prm.check_zero && nt == 0) {  // binary map: any 0 in a real pixel (not padding)?

@@ -116,7 +116,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             mbar_init(&b_empty[s], 1);
         }
         for (int s = 0; s < (int)PR_A_STAGES; ++s) {
-            mbar_init(&a_ready[s], 8);
+            mbar_init(&a_ready[s], LAYOUT >= 2 ? 16 : 8);  // int8 A: all 8 converter warps of both CTAs
             mbar_init(&a_empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -154,18 +154,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     if (A_TER) tma_load_2d(raw + PR_RAW_BYTES, &tmap_a1, &raw_full[rs], kb * 16, arow);
                 }
             }
-        }
-    } else if (warp == PR_W_B) {
-        // ===================== B producer (both CTAs; bytes land on the leader) =====================
-        if (lane == 0) {
-            // both CTAs' halves of B (+ both CTAs' int8 A tiles when A comes straight from TMA)
-            const uint32_t pair_bytes = (uint32_t)bn * PR_BK + (LAYOUT >= 2 ? 2 * PR_A_BYTES : 0);
-            const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
-            const uint64_t b_policy = l2_policy_evict_last();
+        } else if (LAYOUT >= 2 && lane == 0) {
+            // int8 A (dense, or im2col over an NHWC map): this CTA's 128 x 128 tile lands in its A
+            // slot on a LOCAL barrier (raw_full[slot]); the converters sign it in place, then
+            // release it to the MMA issuer through a_ready
             uint32_t t = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int mt = tile / prm.n_tiles, nt = tile - mt * prm.n_tiles;
-                const int brow = nt * bn + (int)rank * bnh;
+                const int mt = tile / prm.n_tiles;
                 const int arow = mt * 2 * PR_BM + (int)rank * PR_BM;
                 int img = 0, oy = 0, ox = 0;
                 if (LAYOUT == 3) {  // first output pixel of this CTA's 128 rows
@@ -175,21 +170,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     ox = rem - oy * prm.conv_ow;
                 }
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
+                    const uint32_t st = t % PR_A_STAGES;
+                    mbar_wait_sleep(&a_empty[st], ((t / PR_A_STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&raw_full[st], PR_A_BYTES);
+                    if (LAYOUT == 2) {  // 128 rows x 128 depth, 128B swizzle = the UMMA tile
+                        tma_load_2d(sA + st * PR_A_BYTES, &tmap_a0, &raw_full[st], kb * PR_BK, arow);
+                    } else {  // implicit GeMM: tap (ky, kx), 128 channels, 128 output pixels
+                        const int tap = kb / prm.conv_cblocks, cb = kb - tap * prm.conv_cblocks;
+                        const int ky = tap / prm.conv_kw, kx = tap - ky * prm.conv_kw;
+                        tma_load_im2col_4d(smem_u32(sA + st * PR_A_BYTES), &tmap_a0, smem_u32(&raw_full[st]),
+                                           cb * 128, ox * prm.conv_stride - prm.conv_pad,
+                                           oy * prm.conv_stride - prm.conv_pad, img, (uint16_t)kx, (uint16_t)ky);
+                    }
+                }
+            }
+        }
+    } else if (warp == PR_W_B) {
+        // ===================== B producer (both CTAs; bytes land on the leader) =====================
+        if (lane == 0) {
+            // both CTAs' halves of B
+            const uint32_t pair_bytes = (uint32_t)bn * PR_BK;
+            const uint32_t b_full0 = mapa_shared(smem_u32(&b_full[0]), 0);
+            const uint64_t b_policy = l2_policy_evict_last();
+            uint32_t t = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                const int nt = tile % prm.n_tiles;
+                const int brow = nt * bn + (int)rank * bnh;
+                for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t st = t % PR_B_STAGES;
                     mbar_wait_sleep(&a_empty[st], ((t / PR_B_STAGES) & 1) ^ 1);  // shared ring: A/B slot free
                     if (leader) mbar_arrive_expect_tx(&b_full[st], pair_bytes);
                     // the weights are re-read for every m tile: keep them in L2 (evict_last)
                     tma_load_2d_pair_hint(smem_u32(sB + st * PR_B_BYTES), &tmap_b, b_full0 + st * 8, kb * PR_BK, brow,
                                           b_policy);
-                    if (LAYOUT == 2) {  // dense int8 A: 128 rows x 128 depth, 128B swizzle = the UMMA tile
-                        tma_load_2d_pair(smem_u32(sA + st * PR_A_BYTES), &tmap_a0, b_full0 + st * 8, kb * PR_BK, arow);
-                    } else if (LAYOUT == 3) {  // implicit GeMM: tap (ky, kx), 128 channels, 128 output pixels
-                        const int tap = kb / prm.conv_cblocks, cb = kb - tap * prm.conv_cblocks;
-                        const int ky = tap / prm.conv_kw, kx = tap - ky * prm.conv_kw;
-                        tma_load_im2col_4d_pair(smem_u32(sA + st * PR_A_BYTES), &tmap_a0, b_full0 + st * 8, cb * 128,
-                                                ox * prm.conv_stride - prm.conv_pad, oy * prm.conv_stride - prm.conv_pad,
-                                                img, (uint16_t)kx, (uint16_t)ky);
-                    }
                 }
             }
         }
@@ -212,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const uint32_t d_tmem = tmem_base + (uint32_t)acc * PR_MAX_BN;
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t sa = t % PR_A_STAGES, sb = t % PR_B_STAGES;
-                    if (LAYOUT < 2) {
+                    {
                         PR_T0();
                         mbar_wait(&a_ready[sa], (t / PR_A_STAGES) & 1);  // latency-critical: poll
                         PR_ACC(w_a);
@@ -245,6 +258,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 atomicAdd(&g_pair_stats[3], (unsigned long long)(clock64() - t_start));
                 atomicAdd(&g_pair_stats[12], (unsigned long long)t);
             }
+        }
+    } else if (warp < 8 && LAYOUT >= 2) {
+        // ===================== int8 A: sign check (both CTAs) =====================
+        // encode_ternary / encode_binary map an int8 value by its sign (core.cpp:13-58): v > 0 is
+        // +1, v < 0 is -1, 0 is 0, so the UMMA must see sign(v), not v.  All 8 warps check each
+        // landed A tile (16 KB, 64 B per thread, conflict-free 16-byte chunks); a chunk holding
+        // a value outside {-1, 0, +1} is rewritten with its signs.  Then the writes are made
+        // visible to the async proxy and the warps arrive on the leader's a_ready.
+        const uint32_t a_ready0 = mapa_shared(smem_u32(&a_ready[0]), 0);
+        const uint32_t total = (uint32_t)((num_tiles - pair + npairs - 1) / npairs) * (uint32_t)prm.kblocks;
+        for (uint32_t t = 0; t < total; ++t) {
+            const uint32_t st = t % PR_A_STAGES;
+            mbar_wait_sleep(&raw_full[st], (t / PR_A_STAGES) & 1);
+            const uint32_t base = smem_u32(sA + st * PR_A_BYTES) + threadIdx.x * 16u;
+            uint4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = lds_v4(base + q * 4096u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (out_of_sign_domain(v[q].x) | out_of_sign_domain(v[q].y) | out_of_sign_domain(v[q].z) |
+                    out_of_sign_domain(v[q].w))
+                    sts_v4(base + q * 4096u, sign_i8x4(v[q].x), sign_i8x4(v[q].y), sign_i8x4(v[q].z),
+                           sign_i8x4(v[q].w));
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(a_ready0 + st * 8);
         }
     } else if (warp < 8) {
         // ===================== converters (both CTAs) =====================

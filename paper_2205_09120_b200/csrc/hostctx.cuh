@@ -44,9 +44,7 @@ class HostCopier {
         const void* src;
         size_t bytes;
     };
-    explicit HostCopier(int threads) : nthreads_(threads < 1 ? 1 : threads) {
-        for (int t = 0; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
-    }
+    explicit HostCopier(int threads) : nthreads_(threads < 1 ? 1 : threads) {}
     ~HostCopier() {
         {
             std::lock_guard<std::mutex> l(mu_);
@@ -56,7 +54,17 @@ class HostCopier {
         for (auto& w : workers_) w.join();
     }
     // Copy every job (each split into one stripe per worker); returns when all are done.
+    // Small rounds are copied on the calling thread (the workers start on the first large one).
     void copy(const Job* jobs, int njobs) {
+        size_t total = 0;
+        for (int j = 0; j < njobs; ++j) total += jobs[j].bytes;
+        if (total < kSmallBytes || nthreads_ == 1) {
+            for (int j = 0; j < njobs; ++j)
+                if (jobs[j].bytes) std::memcpy(jobs[j].dst, jobs[j].src, jobs[j].bytes);
+            return;
+        }
+        if (workers_.empty())
+            for (int t = 0; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
         std::unique_lock<std::mutex> l(mu_);
         jobs_ = jobs;
         njobs_ = njobs;
@@ -65,6 +73,7 @@ class HostCopier {
         cv_.notify_all();
         done_cv_.wait(l, [this] { return left_ == 0; });
     }
+    static constexpr size_t kSmallBytes = 256 << 10;
     static int default_threads() {
         const int hw = (int)std::thread::hardware_concurrency();
         // memcpy pinned -> pageable: 14 GB/s on 1 thread, ~54 GB/s (the PCIe rate) on 8 (host_copy_bw.cu)
@@ -86,7 +95,8 @@ class HostCopier {
                 nj = njobs_;
             }
             for (int j = 0; j < nj; ++j) {
-                const size_t per = (jobs[j].bytes / nthreads_ + 63) & ~size_t(63);  // cache-line stripes
+                // cache-line stripes covering the whole job (ceil, so no byte is left out)
+                const size_t per = ((jobs[j].bytes + nthreads_ - 1) / nthreads_ + 63) & ~size_t(63);
                 const size_t a = per * t < jobs[j].bytes ? per * t : jobs[j].bytes;
                 const size_t b = a + per < jobs[j].bytes ? a + per : jobs[j].bytes;
                 if (b > a)
