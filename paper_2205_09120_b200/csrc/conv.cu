@@ -22,6 +22,10 @@
 
 namespace lb {
 
+#ifndef K4_BLOCKS_PER_SM
+#define K4_BLOCKS_PER_SM 4
+#endif
+
 struct ConvGeom {
     int batch, h, w, c, kh, kw, stride, pad, oh, ow, k;
 };
@@ -162,6 +166,149 @@ __global__ void conv_encode_rows_kernel(int a_binary, const int8_t* __restrict__
     if (saw_zero && zero_flag) atomicOr(zero_flag, 1);
 }
 
+// c % 32 == 0, the encode-once form: a block walks a contiguous range of output
+// rows; every input row it needs is encoded ONCE into a shared-memory ring of
+// kh rows of (plus, minus) words per (pixel, 32-channel group) — the encode
+// ALU work is the input size, not the kh*kw-fold im2col size — and each output
+// word is then a shared-memory lookup.  A per-block table gives, for every
+// (output column ox, word), the tap row ky and the word's offset inside a ring
+// row (pixel ox*s + kx - pad, group); pad and past-the-depth words point at two
+// extra entries (the pad value's words, zeros) through two extra "tap rows".
+// So an output word is ring[slot_of_ky[ky] + offset]: no branches, no
+// divisions.  Output rows leave as 16-byte stores of 4 consecutive words
+// (pitch % 16 == 0), a block's output pixels being consecutive GeMM rows; the
+// next output row's new input row is loaded during the current row's stores.
+__global__ void conv_encode_ring_kernel(int a_binary, const int8_t* __restrict__ fm, ConvGeom g, int pad_value,
+                                        uint8_t* __restrict__ plane0, uint8_t* __restrict__ plane1, long long pitch,
+                                        int* zero_flag) {
+    extern __shared__ __align__(16) uint8_t conv_smem[];
+    const int wpr = (int)(pitch / 4), kwords = g.k / 32, G = g.c / 32;
+    const int row_groups = g.w * G, ring_words = g.kh * row_groups;
+    const int PAD_IDX = ring_words, ZERO_IDX = ring_words + 1;
+    uint32_t* table = reinterpret_cast<uint32_t*>(conv_smem);  // [ox][word]: (tap row << 24) | offset
+    uint32_t* encP = table + g.ow * wpr;                       // ring rows, pad entry, zero entry
+    uint32_t* encM = encP + ring_words + 2;
+    __shared__ int slot_of_ky[258];  // ring-row base of tap row ky (kh: the pad entry, kh + 1: the zero entry)
+    for (int t = threadIdx.x; t < g.ow * wpr; t += blockDim.x) {
+        const int ox = t / wpr, wd = t - ox * wpr;
+        uint32_t e = (uint32_t)(g.kh + 1) << 24;  // past the depth: a zero word
+        if (wd < kwords) {
+            const int k0 = wd * 32, tap = k0 / g.c, c0 = k0 - tap * g.c;
+            const int ky = tap / g.kw, kx = tap - ky * g.kw;
+            const int x = ox * g.stride + kx - g.pad;
+            e = (x >= 0 && x < g.w) ? ((uint32_t)ky << 24) | (uint32_t)(x * G + c0 / 32) : (uint32_t)g.kh << 24;
+        }
+        table[t] = e;
+    }
+    const uint32_t pad_p = pad_value > 0 ? 0xFFFFFFFFu : 0u, pad_m = pad_value < 0 ? 0xFFFFFFFFu : 0u;
+    if (threadIdx.x == 0) {
+        encP[PAD_IDX] = pad_p;
+        encM[PAD_IDX] = pad_m;
+        encP[ZERO_IDX] = 0;
+        encM[ZERO_IDX] = 0;
+        slot_of_ky[g.kh] = PAD_IDX;
+        slot_of_ky[g.kh + 1] = ZERO_IDX;
+    }
+    const uint32_t zero_tap = (uint32_t)(g.kh + 1);
+    const long long orows = (long long)g.batch * g.oh;
+    const long long r_begin = orows * blockIdx.x / gridDim.x, r_end = orows * (blockIdx.x + 1) / gridDim.x;
+    const int wpr4 = wpr / 4, per_row = g.ow * wpr4;
+    bool saw_zero = false;
+    int have_img = -1, have_hi = -1;  // ring holds padded input rows (have_hi - kh, have_hi] of image have_img
+    // next output row's one new input row (stride 1, same image), loaded during this row's stores
+    constexpr int PF = 2;             // groups per thread held in registers (row_groups <= PF * blockDim)
+    uint4 pf[PF][2];
+    int pf_yp = -1;
+    int img = (int)(r_begin / g.oh), oy = (int)(r_begin - (long long)img * g.oh);
+    for (long long orow = r_begin; orow < r_end; ++orow) {
+        const int lo = oy * g.stride, hi = lo + g.kh - 1;  // padded input rows needed (y + pad)
+        int first = lo;
+        if (img == have_img && have_hi >= lo) first = have_hi + 1;
+        __syncthreads();  // the previous row's lookups are done before the ring changes
+        for (int yp = first; yp <= hi; ++yp) {  // encode padded row yp into ring slot yp % kh
+            const int y = yp - g.pad, slot = yp % g.kh;
+            uint32_t* dp = encP + slot * row_groups;
+            uint32_t* dm = encM + slot * row_groups;
+            if (yp == pf_yp) {  // prefetched during the previous row's stores
+#pragma unroll
+                for (int q = 0; q < PF; ++q) {
+                    const int i = threadIdx.x + q * blockDim.x;
+                    if (i < row_groups) {
+                        uint32_t p, m;
+                        encode_word32_regs(pf[q][0], pf[q][1], p, m);
+                        dp[i] = p;
+                        dm[i] = m;
+                    }
+                }
+            } else if (y >= 0 && y < g.h) {
+                const int8_t* src = fm + ((long long)img * g.h + y) * g.w * g.c;
+                for (int i = threadIdx.x; i < row_groups; i += blockDim.x) {
+                    const uint4* q = reinterpret_cast<const uint4*>(src + (long long)i * 32);
+                    uint32_t p, m;
+                    encode_word32_regs(__ldg(q), __ldg(q + 1), p, m);
+                    dp[i] = p;
+                    dm[i] = m;
+                }
+            } else {
+                for (int i = threadIdx.x; i < row_groups; i += blockDim.x) {
+                    dp[i] = pad_p;
+                    dm[i] = pad_m;
+                }
+            }
+        }
+        for (int ky = threadIdx.x; ky < g.kh; ky += blockDim.x) slot_of_ky[ky] = ((lo + ky) % g.kh) * row_groups;
+        have_img = img;
+        have_hi = hi;
+        __syncthreads();
+        // prefetch the next output row's single new input row (stride 1 within an image)
+        pf_yp = -1;
+        if (orow + 1 < r_end && g.stride == 1 && oy + 1 < g.oh && row_groups <= PF * (int)blockDim.x) {
+            const int yn = hi + 1 - g.pad;
+            if (yn >= 0 && yn < g.h) {
+                pf_yp = hi + 1;
+                const int8_t* src = fm + ((long long)img * g.h + yn) * g.w * g.c;
+#pragma unroll
+                for (int q = 0; q < PF; ++q) {
+                    const int i = threadIdx.x + q * blockDim.x;
+                    if (i < row_groups) {
+                        const uint4* qq = reinterpret_cast<const uint4*>(src + (long long)i * 32);
+                        pf[q][0] = __ldg(qq);
+                        pf[q][1] = __ldg(qq + 1);
+                    }
+                }
+            }
+        }
+        uint8_t* out0 = plane0 + orow * g.ow * pitch;
+        uint8_t* out1 = a_binary ? nullptr : plane1 + orow * g.ow * pitch;
+        for (int t = threadIdx.x; t < per_row; t += blockDim.x) {  // t = ox * wpr4 + w4: 4 words
+            const uint4 e4 = *reinterpret_cast<const uint4*>(table + 4 * t);
+            const uint32_t ev[4] = {e4.x, e4.y, e4.z, e4.w};
+            uint32_t P[4], M[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t tap = ev[j] >> 24;
+                const int idx = slot_of_ky[tap] + (int)(ev[j] & 0xFFFFFFu);
+                P[j] = encP[idx];
+                M[j] = encM[idx];
+                // binary maps: a 0 among the values this word takes (im2col's view, core.cpp:23)
+                if (a_binary) saw_zero |= tap != zero_tap && (P[j] | M[j]) != 0xFFFFFFFFu;
+            }
+            const long long off = (long long)t * 16;  // ox * pitch + w4 * 16 (pitch = 16 * wpr4)
+            if (a_binary) {
+                *reinterpret_cast<uint4*>(out0 + off) = make_uint4(M[0], M[1], M[2], M[3]);
+            } else {
+                *reinterpret_cast<uint4*>(out0 + off) = make_uint4(P[0], P[1], P[2], P[3]);
+                *reinterpret_cast<uint4*>(out1 + off) = make_uint4(M[0], M[1], M[2], M[3]);
+            }
+        }
+        if (++oy == g.oh) {
+            oy = 0;
+            ++img;
+        }
+    }
+    if (saw_zero && zero_flag) atomicOr(zero_flag, 1);
+}
+
 __global__ void widen_kernel(const int16_t* __restrict__ in, int32_t* __restrict__ out, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         out[i] = in[i];
@@ -231,7 +378,20 @@ extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int 
     const long long work = (long long)batch * g.oh * g.ow * (pitch / 4);
     const int wpr = (int)(pitch / 4);
     const long long smem = ((wpr * 4LL + 15) & ~15LL) + (long long)kh * w * c;
-    if (c % 32 == 0 && kh < 256 && kw < 256 && smem <= 160 * 1024 && (reinterpret_cast<uintptr_t>(fm) & 15) == 0) {
+    const long long ring_smem = (long long)g.ow * wpr * 4 + 2LL * (kh * w * (c / 32) + 2) * 4;
+    const bool aligned = (reinterpret_cast<uintptr_t>(fm) & 15) == 0 && (reinterpret_cast<uintptr_t>(plane0) & 15) == 0 &&
+                         (a_binary || (reinterpret_cast<uintptr_t>(plane1) & 15) == 0) && (pitch & 15) == 0;
+    if (c % 32 == 0 && kh < 256 && kw < 256 && ring_smem <= 96 * 1024 && aligned && (long long)w * (c / 32) < (1 << 24)) {
+        static SmemOptIn ring_attr;
+        if (ring_smem > 48 * 1024) LB_CUDA_TRY(ring_attr.ensure(conv_encode_ring_kernel, 96 * 1024));
+        const long long orows = (long long)batch * g.oh;
+        // K4_BLOCKS_PER_SM co-resident blocks per SM, each a contiguous run of output rows (it
+        // re-encodes kh - stride input rows at its start)
+        const long long cap = (long long)num_sms() * K4_BLOCKS_PER_SM;
+        const int blocks = (int)(orows < cap ? orows : cap);
+        conv_encode_ring_kernel<<<blocks, 256, (size_t)ring_smem, (cudaStream_t)stream>>>(
+            a_binary, fm, g, pad_value, plane0, plane1, pitch, zero_flag);
+    } else if (c % 32 == 0 && kh < 256 && kw < 256 && smem <= 160 * 1024 && (reinterpret_cast<uintptr_t>(fm) & 15) == 0) {
         static SmemOptIn attr;
         if (smem > 48 * 1024) LB_CUDA_TRY(attr.ensure(conv_encode_rows_kernel, (int)smem));
         const long long orows = (long long)batch * g.oh;

@@ -6,18 +6,28 @@ namespace lb {
 
 __device__ __forceinline__ uint32_t valid_mask32(int nvals) { return nvals >= 32 ? 0xFFFFFFFFu : ((1u << nvals) - 1u); }
 
-// 32 int8 values already in registers (two 16-byte vectors) -> plus / minus words.
+// 32 int8 values already in registers (two 16-byte vectors) -> plus / minus words
+// (bit j <-> value j, by sign: core.cpp:40-58).  Per word: the sign flags
+// ((v >> 7) & 0x01010101) and the positive flags ((low7 != 0) & !sign, bit 7 of
+// ((v & 0x7f..) + 0x7f..) & ~v) sit at bit 0 of each byte; two words' flags go
+// to the top byte of one product, a*0x01020408 + b*0x10204080 (partial
+// products land on distinct bits below 24: no carries), and PRMT collects the
+// four top bytes: ~9 ops per word instead of ~17 for a per-word gather.
+__device__ __forceinline__ uint32_t top8_of_pair(uint32_t a, uint32_t b) { return a * 0x01020408u + b * 0x10204080u; }
 __device__ __forceinline__ void encode_word32_regs(const uint4 lo, const uint4 hi, uint32_t& plus, uint32_t& minus) {
-    plus = 0;
-    minus = 0;
     const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t rn[4], rp[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const uint32_t neg = gather_msb4(v[q]);
-        const uint32_t nz = gather_msb4(nonzero_msb(v[q]));
-        minus |= neg << (4 * q);
-        plus |= (nz & ~neg) << (4 * q);
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t a = v[2 * q], b = v[2 * q + 1];
+        const uint32_t na = (a >> 7) & 0x01010101u, nb = (b >> 7) & 0x01010101u;
+        const uint32_t pa = ((((a & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & ~a & 0x80808080u) >> 7);
+        const uint32_t pb = ((((b & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & ~b & 0x80808080u) >> 7);
+        rn[q] = top8_of_pair(na, nb);
+        rp[q] = top8_of_pair(pa, pb);
     }
+    minus = __byte_perm(__byte_perm(rn[0], rn[1], 0x0073), __byte_perm(rn[2], rn[3], 0x0073), 0x5410);
+    plus = __byte_perm(__byte_perm(rp[0], rp[1], 0x0073), __byte_perm(rp[2], rp[3], 0x0073), 0x5410);
 }
 // 32 (or fewer) consecutive int8 sign values -> plus / minus bit words
 // (bit j <-> value j; LSB-first, core.cpp:13-58).  Vector path when the 32
@@ -26,16 +36,8 @@ __device__ __forceinline__ void encode_word32(const int8_t* src, int nvals, uint
     plus = 0;
     minus = 0;
     if (nvals == 32 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
-        const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-        const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t neg = gather_msb4(v[q]);
-            const uint32_t nz = gather_msb4(nonzero_msb(v[q]));
-            minus |= neg << (4 * q);
-            plus |= (nz & ~neg) << (4 * q);
-        }
+        encode_word32_regs(__ldg(reinterpret_cast<const uint4*>(src)), __ldg(reinterpret_cast<const uint4*>(src) + 1),
+                           plus, minus);
     } else {
         for (int j = 0; j < nvals; ++j) {
             const int8_t x = src[j];

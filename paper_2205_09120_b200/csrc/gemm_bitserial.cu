@@ -22,6 +22,14 @@
 namespace lb {
 
 constexpr int K2_BM = 128, K2_BN = 128, K2_KC = 8, K2_LD = 132;  // K2_LD: padded row length (words)
+// Depth words unrolled per step of the inner loop.  Fully unrolled, TNN's four
+// operand sets for all 8 words hoist into 255 registers and spill (1 CTA per
+// SM); not unrolled it takes 128 registers, 2 CTAs per SM: c5-shaped TNN 129.9
+// -> 141.0 TOPS, 0.947 of the TNN POPC peak (unroll 2: 177 registers, 129.2;
+// tools/k2_time.py).  BNN / TBN stay fully unrolled (126 / 172 registers).
+#ifndef K2_TNN_UNROLL
+#define K2_TNN_UNROLL 1
+#endif
 
 template <int MODE>  // 0 = BNN, 1 = TNN, 2 = TBN
 __global__ void __launch_bounds__(256) gemm_bitserial_kernel(const uint8_t* __restrict__ a0,
@@ -32,6 +40,7 @@ __global__ void __launch_bounds__(256) gemm_bitserial_kernel(const uint8_t* __re
                                                              int16_t* __restrict__ c, long long ldc) {
     constexpr bool A_TER = MODE != 0;
     constexpr bool B_TER = MODE == 1;
+    constexpr int UW = MODE == 1 ? K2_TNN_UNROLL : K2_KC;
     __shared__ __align__(16) uint32_t As_s[2][K2_KC][K2_LD];
     __shared__ __align__(16) uint32_t As_n[A_TER ? 2 : 1][K2_KC][K2_LD];
     __shared__ __align__(16) uint32_t Bs_s[2][K2_KC][K2_LD];
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(256) gemm_bitserial_kernel(const uint8_t* __re
     for (int st = 0; st < nstages; ++st) {
         const int buf = st & 1;
         if (st + 1 < nstages) load_global(st + 1);
-#pragma unroll
+#pragma unroll UW
         for (int w = 0; w < K2_KC; ++w) {
             uint32_t as[8], an[8], bs[8], bn[8];
             *reinterpret_cast<uint4*>(&as[0]) = *reinterpret_cast<const uint4*>(&As_s[buf][w][ty * 4]);

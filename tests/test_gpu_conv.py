@@ -192,3 +192,20 @@ def test_conv_halo_geometries(lb, port, mode):
         for img in range(b):
             want = port.direct_conv(fm[img], mode == BNN, wt, ksz, ksz, 1, pad)
             assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, ch, cout, ksz, pad, img)
+
+
+@pytest.mark.parametrize("ch", [32, 40])
+def test_conv_binary_zero_only_where_sampled(lb, port, ch):
+    """ZeroInBinaryInput follows im2col's view (conv.cpp:9-31, core.cpp:23): a 0 in a
+    column no window reads (w = 8, 3x3, stride 2, no padding: column 7) is not an
+    error; a 0 in a sampled pixel is.  K4's encode-once ring (c % 32 == 0) and its
+    per-word kernel (other c)."""
+    fm = port.generate(1, 58, 0, 9 * 8, ch).reshape(1, 9, 8, ch)
+    wt = port.generate(1, 58, 1, 9 * ch, 8)
+    w = weights_for(lb, wt, BNN)
+    fm[0, 4, 7, 3] = 0
+    got = lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, w, 3, 3, 2, 0, kernel=1).cpu().numpy()
+    assert (got[0].astype(np.int32) == port.conv2d_lowbit(BNN, fm[0], True, wt, True, 3, 3, 2, 0)).all()
+    fm[0, 4, 6, 3] = 0
+    with pytest.raises(lb.ZeroInBinaryInput):
+        lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, w, 3, 3, 2, 0, kernel=1)
