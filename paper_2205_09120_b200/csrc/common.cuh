@@ -158,6 +158,11 @@ LB_DEV void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int 
 
 // Make generic-proxy shared-memory writes visible to the async proxy
 // (tensor core operand reads, TMA stores).
+// Named barrier over `count` threads (a multiple of 32): waiting warps block in
+// hardware without issuing, unlike an mbarrier wait loop.
+LB_DEV void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 LB_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------

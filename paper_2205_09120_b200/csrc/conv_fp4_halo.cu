@@ -274,10 +274,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         for (int nt = 0; nt < prm.n_tiles; ++nt)
             for (int i = 0; i < my_tiles; ++i, ++t) {
                 const uint32_t rs = t % raw_st, fs = t % f4_st;
-                h7_wait(dbg, &raw_full[rs], (t / raw_st) & 1);
-                if (cw == 0 && lane == 0) H7_TRACE(1, t);
-                h7_wait(dbg, &a_empty[fs], ((t / f4_st) & 1) ^ 1);
-                if (cw == 0 && lane == 0) H7_TRACE(2, t);
+                if (cw == 0) {  // one converter warp waits; the others block on a named barrier
+                    h7_wait(dbg, &raw_full[rs], (t / raw_st) & 1);
+                    if (lane == 0) H7_TRACE(1, t);
+                    h7_wait(dbg, &a_empty[fs], ((t / f4_st) & 1) ^ 1);
+                    if (lane == 0) H7_TRACE(2, t);
+                }
+                named_bar_sync(3, 32 * H7_NCONV);
                 if (convert)
                     for (int cb = 0; cb < CB; ++cb) {
                         const uint32_t src = smem_u32(sRaw + rs * raw_stage + cb * raw_cb) + chunk * 16;
@@ -429,7 +432,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 const int img = ct / prm.tpi;
                 const int oy = (ct - img * prm.tpi) * prm.R + ry;
                 const bool store_ok = ct < prm.ctiles && oy < prm.oh && !(prm.dbg & 1);
-                if (!(prm.dbg & 64)) h7_wait(prm.dbg, &tmem_full[acc], acc_phase);
+                // one warp of the group waits on the mbarrier, the other seven block on a named
+                // barrier: sixteen wait loops cost issue slots the converters need
+                if (!(prm.dbg & 64) && (warp & 7) == 0) h7_wait(prm.dbg, &tmem_full[acc], acc_phase);
+                named_bar_sync(1 + tgrp, 256);
                 tc_fence_after();
                 if (wq == 0 && lane == 0) H7_TRACE(7, u);
                 if (prm.dbg & 128) {  // timing experiment: drain nothing

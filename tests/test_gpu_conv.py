@@ -209,3 +209,24 @@ def test_conv_binary_zero_only_where_sampled(lb, port, ch):
     fm[0, 4, 6, 3] = 0
     with pytest.raises(lb.ZeroInBinaryInput):
         lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, w, 3, 3, 2, 0, kernel=1)
+
+
+@pytest.mark.parametrize("mode", [TNN, TBN])
+def test_conv_halo_strips(lb, port, mode):
+    """K7 walks each CTA's contiguous strip of CTA tiles with a sliding window of
+    input rows (each row converted once per strip; a new image restarts the
+    window).  Batches large enough that strips span several tiles and cross
+    image boundaries at different steps in the two CTAs of a pair, for every
+    position pitch, two channel blocks and two n tiles."""
+    da, db = mode_dists(mode)
+    cases = [(64, 9, 9, 128, 64, 3, 1), (40, 20, 20, 256, 48, 3, 1), (24, 30, 56, 128, 128, 3, 1),
+             (12, 33, 100, 128, 40, 3, 1), (48, 12, 12, 128, 256, 3, 0), (20, 15, 28, 128, 32, 5, 2)]
+    for i, (b, h, w, ch, cout, ksz, pad) in enumerate(cases):
+        assert lb.conv_select(mode, False, b, h, w, ch, cout, ksz, ksz, 1, pad) == lb.CONV_PATH_HALO_FP4
+        fm = port.generate(da, 170 + i, 0, b * h * w, ch).reshape(b, h, w, ch)
+        wt = port.generate(db, 170 + i, 1, ksz * ksz * ch, cout)
+        got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), False, weights_for(lb, wt, mode), ksz, ksz, 1,
+                               pad).cpu().numpy()
+        for img in range(b):
+            want = port.direct_conv(fm[img], False, wt, ksz, ksz, 1, pad)
+            assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, ch, cout, ksz, pad, img)
