@@ -609,6 +609,8 @@ def cpp_dropin_e2e(mode, M, N, K, seed, iters=3):
         return {"value": d["TOPS"], "unit": "TOPS", "ms_per_step": d["ms_mean"],
                 "h2d_bytes_per_step": d["h2d_bytes_per_call"], "d2h_bytes_per_step": d["d2h_bytes_per_call"],
                 "equal_device_path": d["equal_device_path"],
+                # the zero-initialised Int16Matrix the reference API returns by value, allocated alone
+                "result_alloc_ms": d.get("result_alloc_ms_median"),
                 "path": "C++ drop-in lowbit::gemm_lowbit(mode, TernaryPackedMatrix, PackedB, dims) -> Int16Matrix, "
                         "std::vector buffers, host clock, result allocation included"}
     except Exception as e:

@@ -140,6 +140,22 @@ int main(int argc, char** argv) {
         ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
         if (c.values.size() != (size_t)m * n) return 3;
     }
+    // what the reference API itself costs here: gemm_lowbit returns its Int16Matrix by value
+    // (gemm.hpp:78-81), a zero-initialised std::vector of m*n int16 — the same allocation, timed alone
+    std::vector<double> alloc_ms;
+    for (int i = 0; i < iters; ++i) {
+        auto t0 = std::chrono::steady_clock::now();
+        {
+            Int16Matrix c;
+            c.rows = m;
+            c.cols = n;
+            c.values.assign((size_t)m * n, 0);
+            if (c.values[(size_t)m * n / 2] != 0) return 5;
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        alloc_ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
+    std::sort(alloc_ms.begin(), alloc_ms.end());
     std::sort(ms.begin(), ms.end());
     double mean = 0;
     for (double x : ms) mean += x;
@@ -148,7 +164,9 @@ int main(int argc, char** argv) {
     const size_t h2d = (size_t)m * ((k + 7) / 8) * (a_ter ? 2 : 1), d2h = (size_t)m * n * 2;
     std::printf(
         "{\"mode\": %d, \"m\": %d, \"n\": %d, \"k\": %d, \"iters\": %d, \"ms_mean\": %.3f, \"ms_median\": %.3f, "
-        "\"TOPS\": %.3f, \"h2d_bytes_per_call\": %zu, \"d2h_bytes_per_call\": %zu, \"equal_device_path\": %s}\n",
-        mode, m, n, k, iters, mean, ms[ms.size() / 2], ops / (mean * 1e-3) / 1e12, h2d, d2h, equal ? "true" : "false");
+        "\"TOPS\": %.3f, \"h2d_bytes_per_call\": %zu, \"d2h_bytes_per_call\": %zu, \"equal_device_path\": %s, "
+        "\"result_alloc_ms_median\": %.3f}\n",
+        mode, m, n, k, iters, mean, ms[ms.size() / 2], ops / (mean * 1e-3) / 1e12, h2d, d2h, equal ? "true" : "false",
+        alloc_ms[alloc_ms.size() / 2]);
     return equal ? 0 : 4;
 }
