@@ -317,7 +317,10 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": f"low-bit GeMM TOPS (MAC=2 ops), {MODE_NAME[mode]} {args.config}",
         "value": v, "unit": "TOPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ops / (v * 1e12) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": ops / (v * 1e12) * 1e3,
+        "ms_per_step_note": "extrapolated: the whole config's ops at the rate measured on a bounded row sample "
+                            "(each step times one sample; rows are independent, gemm.cpp:35-51)",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8 bit-planes / int16", "data": "synthetic (counter-based generator)",
         "config": {"workload": f"{args.config}: {MODE_NAME[mode]} M={M} N={N} K={K}, reference CPU path "
                                f"extrapolated from a bounded row sample per step"},
