@@ -616,8 +616,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             tile_of(i, mt, nt);
             const int row0 = mt * 2 * F4_BM + (int)rank * F4_BM + wq * 32;
             {
+                // one epilogue warp waits on the mbarrier; the others block on a named barrier
+                // (wait loops in every warp cost issue slots)
                 F4_T0();
-                mbar_wait_sleep(&tmem_full[acc], acc_phase);
+                if (ewarp == 0) mbar_wait_sleep(&tmem_full[acc], acc_phase);
+                named_bar_sync(1, 32 * EPI_W);
                 F4_ACC(w_ep);
             }
             F4_T0();

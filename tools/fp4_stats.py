@@ -6,7 +6,7 @@ import torch
 import paper_2205_09120_b200 as lb
 L = lb._lib
 M, N, K = int(os.environ.get("M", 1048576)), int(os.environ.get("N", 1024)), int(os.environ.get("K", 2048))
-a = lb.generate(0, 47, 0, M, K); ap = lb.encode_ternary(a, layout=2); del a
+a = lb.generate(0, 47, 0, M, K); ap = lb.encode_ternary(a, layout=int(os.environ.get("LAYOUT", 2))); del a
 w = lb.prepare_weights(lb.pack_b(lb.encode_ternary(lb.generate(0, 47, 1, K, N))))
 c = torch.empty((M, N), dtype=torch.int16, device="cuda")
 for _ in range(3):
