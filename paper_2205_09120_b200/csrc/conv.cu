@@ -326,8 +326,8 @@ lowbit_status launch_conv_fp4(const int8_t* fm, int batch, int h, int w, int cch
 bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int kw, int stride, int pad,
                        long long batch);
 lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int pad,
-                               int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
-                               int* zero_flag, cudaStream_t stream);
+                               int check_zero, int pad_value, const void* weights, int b_ternary, int cout,
+                               int16_t* out, int* zero_flag, cudaStream_t stream);
 lowbit_status launch_conv_pair_im2col(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int stride,
                                       int pad, const void* weights, int b_ternary, int cout, int16_t* out,
                                       cudaStream_t stream);
@@ -415,14 +415,16 @@ extern "C" size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int 
 }
 
 // Which conv kernel lowbit_conv2d runs (pointers assumed aligned; host logic only):
-//   K7 fused halo conv — stride 1, the padded row fits 128 pixels, c % 128 == 0, padding that
-//      reads as 0 (ternary map or no padding), the filter + two halo stages fit in shared memory;
-//   K6 fp4 implicit GeMM over a packed fp4 copy of the map — same padding rule, any stride (needs
-//      the workspace);
+//   K7 fused halo conv — stride 1, the padded row fits 128 pixels, c % 128 == 0, the filter + two
+//      halo stages fit in shared memory; any padding (binary maps padded with +-1 get the pad
+//      codes written by the converters; a BNN map padded with 0 must raise ZeroInBinaryInput and
+//      takes K4, decided in lowbit_conv2d where the pad value is known);
+//   K6 fp4 implicit GeMM over a packed fp4 copy of the map — padding that reads as 0 (ternary map
+//      or no padding), any stride (needs the workspace);
 //   int8 implicit GeMM (TMA im2col over the int8 map) — TNN/TBN, c % 128 == 0, padding reads 0;
 //   else K4 (fused im2col + encode) + lowbit_gemm.
-// BNN maps padded with +-1 always take the last path: TMA's out-of-bounds fill is 0 and a 0
-// activation must raise ZeroInBinaryInput (conv.cpp:13, core.cpp:23).
+// TMA's out-of-bounds fill is 0, so the im2col paths (K6, int8) keep binary maps padded with
+// +-1 on K4 (conv.cpp:13).
 extern "C" int lowbit_conv_select(int mode, int fm_binary, int batch, int h, int w, int c, int cout, int kh, int kw,
                                   int stride, int padding, int kernel, int has_workspace) {
     const long long rows = lowbit_conv_rows(batch, h, w, kh, kw, stride, padding);
@@ -456,12 +458,16 @@ extern "C" lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, in
     const bool aligned = (reinterpret_cast<uintptr_t>(fm) & 15) == 0 &&
                          (reinterpret_cast<uintptr_t>(weights) & 255) == 0 &&
                          (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    const int path = aligned ? lowbit_conv_select(mode, fm_binary, batch, h, w, c, cout, kh, kw, stride, padding,
-                                                  kernel, workspace != nullptr)
-                             : LOWBIT_CONV_PATH_ENCODE_GEMM;
+    int path = aligned ? lowbit_conv_select(mode, fm_binary, batch, h, w, c, cout, kh, kw, stride, padding, kernel,
+                                            workspace != nullptr)
+                       : LOWBIT_CONV_PATH_ENCODE_GEMM;
+    // a BNN map padded with 0 holds zeros im2col encodes: K4 raises ZeroInBinaryInput (core.cpp:23)
+    if (path == LOWBIT_CONV_PATH_HALO_FP4 && mode == LOWBIT_BNN && fm_binary && padding > 0 && binary_pad_value == 0)
+        path = LOWBIT_CONV_PATH_ENCODE_GEMM;
     if (path == LOWBIT_CONV_PATH_HALO_FP4)
-        return lb::launch_conv_halo(fm, batch, h, w, c, kh, kw, padding, mode == LOWBIT_BNN && fm_binary, weights,
-                                    b_ternary, cout, out, zero_flag, (cudaStream_t)stream);
+        return lb::launch_conv_halo(fm, batch, h, w, c, kh, kw, padding, mode == LOWBIT_BNN && fm_binary,
+                                    fm_binary ? binary_pad_value : 0, weights, b_ternary, cout, out, zero_flag,
+                                    (cudaStream_t)stream);
     if (path == LOWBIT_CONV_PATH_IMPLICIT_FP4)
         return lb::launch_conv_fp4(fm, batch, h, w, c, kh, kw, stride, padding, mode == LOWBIT_BNN && fm_binary,
                                    weights, b_ternary, cout, out, workspace, zero_flag, (cudaStream_t)stream);

@@ -76,6 +76,8 @@ struct HaloParams {
     int nacc, acc_cols;        // TMEM accumulators and their column stride
     int k33;                   // 3x3 filter over one channel block: the unrolled issue loop
     int check_zero;            // binary map: a 0 activation sets *zero_flag (core.cpp:23)
+    uint32_t pad_word;         // binary map padded with +-1 (binary_pad_value, conv.cpp:13): 4 int8 pad values;
+                               // 0 when the padding reads as 0 (the TMA's out-of-bounds fill)
     int dbg;                   // timing experiments (LOWBIT_HALO_DEBUG): 1 no stores, 2 no MMAs, 4 no conversion,
                                // 8 no TMEM loads, 16 no staging stores,
                                // 64 epilogue ignores tmem_full, 128 epilogue drains nothing, 32 trace,
@@ -143,7 +145,7 @@ LB_DEV void h7_wait(int dbg, uint64_t* bar, uint32_t parity) {
     else mbar_wait_sleep(bar, parity);
 }
 
-template <int NEPI>
+template <int NEPI, bool PADFILL>  // PADFILL: a binary map padded with +-1 (the pad codes are written)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     conv_fp4_halo_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_raw,
                          const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
@@ -310,6 +312,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                             sts_v2(dst + (uint32_t)j * 64u, h7_pack8_sign(v.x, v.y), h7_pack8_sign(v.z, v.w));
                         }
                     }
+                if (PADFILL && convert) {
+                    // binary map padded with +-1: the TMA filled out-of-image pixels with 0; overwrite
+                    // this lane's padding positions (after its own conversion stores) with the pad codes
+                    const int ct = (pair + i * npairs) * 2 + (int)rank;
+                    const int img = ct / tpi;
+                    const int ytop = (ct - img * tpi) * R - prm.pad;  // image row of halo row 0
+                    const uint32_t pad_code = h7_pack8(prm.pad_word, prm.pad_word);  // 8 e2m1 pad codes
+                    for (int cb = 0; cb < CB; ++cb) {
+                        const uint32_t dst = smem_u32(sF4 + fs * f4_stage + cb * f4_cb) + swz;
+                        for (int j = j0; j < npos; j += STEP) {
+                            const int y = ytop + (j >> lp), x = (j & (P - 1)) - prm.pad;
+                            if (y < 0 || y >= prm.h || x < 0 || x >= prm.w) sts_v2(dst + (uint32_t)j * 64u, pad_code, pad_code);
+                        }
+                    }
+                }
                 if (prm.check_zero && nt == 0) {  // binary map: any 0 in a real pixel (not padding)?
                     const int ct = (pair + i * npairs) * 2 + (int)rank;
                     const int img = ct / tpi;
@@ -578,7 +595,7 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
 // filter + two raw and two fp4 halo stages that fit in shared memory.
 bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int kw, int stride, int pad,
                        long long batch) {
-    if (!(pad == 0 || !fm_binary)) return false;
+    (void)fm_binary;  // binary maps padded with +-1: the converters write the pad codes
     const HaloGeom g = halo_geom(h, w, c, cout, kh, kw, stride, pad);
     if (!g.ok) return false;
     const long long tpi = (h + 2 * pad - kh + 1 + g.R - 1) / g.R;
@@ -586,8 +603,8 @@ bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int
 }
 
 lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int pad,
-                               int check_zero, const void* weights, int b_ternary, int cout, int16_t* out,
-                               int* zero_flag, cudaStream_t stream) {
+                               int check_zero, int pad_value, const void* weights, int b_ternary, int cout,
+                               int16_t* out, int* zero_flag, cudaStream_t stream) {
     const HaloGeom g = halo_geom(h, w, cch, cout, kh, kw, 1, pad);
     if (!g.ok) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv halo kernel: unsupported shape");
     const int oh = h + 2 * pad - kh + 1, ow = w + 2 * pad - kw + 1;
@@ -624,6 +641,7 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     prm.acc_cols = prm.nacc == 3 ? (int)H7_SF_COL / 3 : H7_MAX_BN;
     prm.k33 = kh == 3 && kw == 3 && prm.cblocks == 1;
     prm.check_zero = check_zero;
+    prm.pad_word = pad > 0 ? (pad_value > 0 ? 0x01010101u : (pad_value < 0 ? 0xFFFFFFFFu : 0u)) : 0u;
     static const int dbg = lb::tuning_env("LOWBIT_HALO_DEBUG") ? atoi(lb::tuning_env("LOWBIT_HALO_DEBUG")) : 0;
     prm.dbg = dbg;
     prm.out = out;
@@ -637,9 +655,11 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
     if (!make_map_nhwc_box(&mraw, fm, batch, h, w, cch, (uint32_t)g.P, (uint32_t)g.rows_h))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the feature-map halo");
-    auto kern = g.nepi == 16 ? conv_fp4_halo_kernel<16> : conv_fp4_halo_kernel<8>;
-    static SmemOptIn attr[2];
-    LB_CUDA_TRY(attr[g.nepi == 16].ensure(kern, H7_SMEM));
+    const bool fill = prm.pad_word != 0;
+    auto kern = g.nepi == 16 ? (fill ? conv_fp4_halo_kernel<16, true> : conv_fp4_halo_kernel<16, false>)
+                             : (fill ? conv_fp4_halo_kernel<8, true> : conv_fp4_halo_kernel<8, false>);
+    static SmemOptIn attr[2][2];
+    LB_CUDA_TRY(attr[g.nepi == 16][fill].ensure(kern, H7_SMEM));
     const int pairs = prm.ptiles < num_sms() / 2 ? prm.ptiles : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);

@@ -106,8 +106,10 @@ def test_conv_select_paths():
     assert sel(L.TNN, False, 3, 8, 7, 128, 96, 3, 3, 2, 1, has_workspace=False) == lb.CONV_PATH_IMPLICIT_I8
     # padded row wider than 128 pixels: K6
     assert sel(L.TNN, False, 1, 2, 130, 128, 24, 3, 3, 1, 1) == lb.CONV_PATH_IMPLICIT_FP4
-    # BNN map padded with +-1, or c not a multiple of 128: K4 encode + GeMM
-    assert sel(L.BNN, True, 64, 56, 56, 128, 128, 3, 3, 1, 1) == lb.CONV_PATH_ENCODE_GEMM
+    # a binary map padded with +-1: K7 writes the pad codes (stride 2: K6 / int8 im2col cannot, K4 does);
+    # c not a multiple of 128: K4 encode + GeMM
+    assert sel(L.BNN, True, 64, 56, 56, 128, 128, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
+    assert sel(L.BNN, True, 3, 8, 7, 128, 96, 3, 3, 2, 1) == lb.CONV_PATH_ENCODE_GEMM
     assert sel(L.TNN, False, 1, 9, 9, 64, 32, 3, 3, 1, 1) == lb.CONV_PATH_ENCODE_GEMM
     # the int8 kernel request skips the fp4 ones; the bit-serial request takes the bit path
     assert sel(L.TNN, False, 64, 56, 56, 128, 128, 3, 3, 1, 1, kernel=L.KERNEL_TENSOR_I8) == lb.CONV_PATH_IMPLICIT_I8

@@ -230,3 +230,31 @@ def test_conv_halo_strips(lb, port, mode):
         for img in range(b):
             want = port.direct_conv(fm[img], False, wt, ksz, ksz, 1, pad)
             assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, ch, cout, ksz, pad, img)
+
+
+@pytest.mark.parametrize("mode", [BNN, TBN, TNN])
+def test_conv_halo_binary_padding(lb, port, mode):
+    """K7 on binary maps padded with binary_pad_value (conv.cpp:13): the TMA fills
+    out-of-image pixels with 0 and the converters overwrite them with the pad
+    value's codes.  +1 and -1 for every mode, 0 for TBN / TNN (encoded ternary:
+    allowed); a BNN map padded with 0 still raises ZeroInBinaryInput (K4)."""
+    da, db = mode_dists(mode)
+    cases = [(2, 9, 9, 128, 64, 3, 1), (3, 14, 20, 128, 40, 3, 1), (1, 7, 30, 128, 32, 5, 2), (2, 9, 9, 256, 64, 3, 1),
+             (4, 6, 50, 128, 48, 3, 1)]
+    for i, (b, h, w, ch, cout, ksz, pad) in enumerate(cases):
+        assert lb.conv_select(mode, True, b, h, w, ch, cout, ksz, ksz, 1, pad) == lb.CONV_PATH_HALO_FP4
+        fm = port.generate(1, 190 + i, 0, b * h * w, ch).reshape(b, h, w, ch)  # binary map
+        wt = port.generate(db, 190 + i, 1, ksz * ksz * ch, cout)
+        wts = weights_for(lb, wt, mode)
+        for pv in ((1, -1) if mode == BNN else (1, -1, 0)):
+            got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), True, wts, ksz, ksz, 1, pad,
+                                   binary_pad_value=pv).cpu().numpy()
+            for img in range(b):
+                want = port.direct_conv(fm[img], True, wt, ksz, ksz, 1, pad, pv)
+                assert (got[img].astype(np.int32) == want).all(), (mode, pv, b, h, w, ch, cout, ksz, pad, img)
+    if mode == BNN:
+        fm = port.generate(1, 199, 0, 2 * 9 * 9, 128).reshape(2, 9, 9, 128)
+        wt = port.generate(1, 199, 1, 9 * 128, 64)
+        with pytest.raises(lb.ZeroInBinaryInput):
+            lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, weights_for(lb, wt, BNN), 3, 3, 1, 1,
+                             binary_pad_value=0)

@@ -8,5 +8,3 @@ for r in 1 2; do
   echo -n "B " >> gpurun_out/k7_time.log; KERNELS=2 timeout 120 python tools/conv_c4_time.py >> gpurun_out/k7_time.log 2>&1
   if [ -f paper_2205_09120_b200/build_c/liblowbit_c.so ]; then echo -n "C " >> gpurun_out/k7_time.log; LOWBIT_LIB=paper_2205_09120_b200/build_c/liblowbit_c.so KERNELS=2 timeout 120 python tools/conv_c4_time.py >> gpurun_out/k7_time.log 2>&1; fi
 done
-LOWBIT_LIB=paper_2205_09120_b200/build_t/liblowbit_t.so LOWBIT_HALO_DEBUG=32 timeout 120 python tools/halo_trace.py > gpurun_out/k7_trace2.log 2>&1
-for d in ${DBG_LIST:-4}; do echo -n "dbg $d: " >> gpurun_out/k7_dbg2.log; LOWBIT_LIB=paper_2205_09120_b200/build_t/liblowbit_t.so LOWBIT_HALO_DEBUG=$d KERNELS=2 timeout 120 python tools/conv_c4_time.py 2>&1 | tail -1 >> gpurun_out/k7_dbg2.log; done
