@@ -145,12 +145,16 @@ LB_DEV void h7_wait(int dbg, uint64_t* bar, uint32_t parity) {
     else mbar_wait_sleep(bar, parity);
 }
 
-template <int NEPI, bool PADFILL>  // PADFILL: a binary map padded with +-1 (the pad codes are written)
+// FLAGS bit 0 (PADFILL): a binary map padded with +-1 — the converters write the pad codes;
+// bit 1 (CHECKZ): a binary BNN map — a 0 in a real pixel raises ZeroInBinaryInput (core.cpp:23).
+// Both are folded into the converters' load/convert batch.
+template <int NEPI, int FLAGS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     conv_fp4_halo_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_raw,
                          const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
                          const HaloParams prm) {
     constexpr int H7_W_CONV = NEPI, H7_W_PROD = H7_W_CONV + H7_NCONV, H7_W_MMA = H7_W_PROD + 1;
+    constexpr bool PADFILL = (FLAGS & 1) != 0, CHECKZ = (FLAGS & 2) != 0;
     if (prm.dbg & 32768) return;  // launch-overhead probe
 
     if ((prm.dbg & 32) && threadIdx.x == 0) atomicMin(&g_halo_phase[0], h7_gtime());
@@ -283,6 +287,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     if (lane == 0) H7_TRACE(2, t);
                 }
                 named_bar_sync(3, 32 * H7_NCONV);
+                int ytop = 0;  // image row of halo row 0 (binary maps: padding / zero checks)
+                if (PADFILL || CHECKZ) {
+                    const int ct = (pair + i * npairs) * 2 + (int)rank;
+                    const int img = ct / tpi;
+                    ytop = (ct >= ctiles ? 0 : (ct - img * tpi) * R) - prm.pad;  // odd tail: the box at row 0
+                }
+                const bool chk = CHECKZ && nt == 0;
                 if (convert)
                     for (int cb = 0; cb < CB; ++cb) {
                         const uint32_t src = smem_u32(sRaw + rs * raw_stage + cb * raw_cb) + chunk * 16;
@@ -292,6 +303,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                             uint4 v[8];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) v[q] = lds_v4(src + raw_off(jb + STEP * q));
+                            if (PADFILL || chk) {
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    const int j = jb + STEP * q;
+                                    const int y = ytop + (j >> lp), x = (j & (P - 1)) - prm.pad;
+                                    const bool real = (unsigned)y < (unsigned)prm.h && (unsigned)x < (unsigned)prm.w;
+                                    if (chk && real && !h7_all_nonzero(v[q])) zero = true;
+                                    if (PADFILL && !real) v[q] = make_uint4(prm.pad_word, prm.pad_word, prm.pad_word, prm.pad_word);
+                                }
+                            }
                             uint32_t bad = 0;
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
@@ -308,39 +329,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                         }
                         for (int q = 0; q < nrem; ++q) {
                             const int j = j0 + nfull * 8 * STEP + STEP * q;
-                            const uint4 v = lds_v4(src + raw_off(j));
+                            uint4 v = lds_v4(src + raw_off(j));
+                            if (PADFILL || chk) {
+                                const int y = ytop + (j >> lp), x = (j & (P - 1)) - prm.pad;
+                                const bool real = (unsigned)y < (unsigned)prm.h && (unsigned)x < (unsigned)prm.w;
+                                if (chk && real && !h7_all_nonzero(v)) zero = true;
+                                if (PADFILL && !real) v = make_uint4(prm.pad_word, prm.pad_word, prm.pad_word, prm.pad_word);
+                            }
                             sts_v2(dst + (uint32_t)j * 64u, h7_pack8_sign(v.x, v.y), h7_pack8_sign(v.z, v.w));
                         }
                     }
-                if (PADFILL && convert) {
-                    // binary map padded with +-1: the TMA filled out-of-image pixels with 0; overwrite
-                    // this lane's padding positions (after its own conversion stores) with the pad codes
-                    const int ct = (pair + i * npairs) * 2 + (int)rank;
-                    const int img = ct / tpi;
-                    const int ytop = (ct - img * tpi) * R - prm.pad;  // image row of halo row 0
-                    const uint32_t pad_code = h7_pack8(prm.pad_word, prm.pad_word);  // 8 e2m1 pad codes
-                    for (int cb = 0; cb < CB; ++cb) {
-                        const uint32_t dst = smem_u32(sF4 + fs * f4_stage + cb * f4_cb) + swz;
-                        for (int j = j0; j < npos; j += STEP) {
-                            const int y = ytop + (j >> lp), x = (j & (P - 1)) - prm.pad;
-                            if (y < 0 || y >= prm.h || x < 0 || x >= prm.w) sts_v2(dst + (uint32_t)j * 64u, pad_code, pad_code);
-                        }
-                    }
-                }
-                if (prm.check_zero && nt == 0) {  // binary map: any 0 in a real pixel (not padding)?
-                    const int ct = (pair + i * npairs) * 2 + (int)rank;
-                    const int img = ct / tpi;
-                    const int y0 = (ct - img * tpi) * R;
-                    if (ct < ctiles)
-                        for (int cb = 0; cb < CB; ++cb) {
-                            const uint32_t src = smem_u32(sRaw + rs * raw_stage + cb * raw_cb) + chunk * 16;
-                            for (int j = j0; j < npos; j += STEP) {
-                                const int y = y0 - prm.pad + (j >> lp), x = (j & (P - 1)) - prm.pad;
-                                if (y >= 0 && y < prm.h && x >= 0 && x < prm.w && !h7_all_nonzero(lds_v4(src + raw_off(j))))
-                                    zero = true;
-                            }
-                        }
-                }
                 if (cw == 0 && lane == 0) H7_TRACE(15, t);
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -655,11 +653,15 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the conv filter");
     if (!make_map_nhwc_box(&mraw, fm, batch, h, w, cch, (uint32_t)g.P, (uint32_t)g.rows_h))
         return lbhost::set_error(LOWBIT_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the feature-map halo");
-    const bool fill = prm.pad_word != 0;
-    auto kern = g.nepi == 16 ? (fill ? conv_fp4_halo_kernel<16, true> : conv_fp4_halo_kernel<16, false>)
-                             : (fill ? conv_fp4_halo_kernel<8, true> : conv_fp4_halo_kernel<8, false>);
-    static SmemOptIn attr[2][2];
-    LB_CUDA_TRY(attr[g.nepi == 16][fill].ensure(kern, H7_SMEM));
+    const int flags = (prm.pad_word != 0 ? 1 : 0) | (check_zero ? 2 : 0);
+    using KernT = decltype(&conv_fp4_halo_kernel<16, 0>);
+    const KernT kerns[2][4] = {{conv_fp4_halo_kernel<8, 0>, conv_fp4_halo_kernel<8, 1>, conv_fp4_halo_kernel<8, 2>,
+                                conv_fp4_halo_kernel<8, 3>},
+                               {conv_fp4_halo_kernel<16, 0>, conv_fp4_halo_kernel<16, 1>, conv_fp4_halo_kernel<16, 2>,
+                                conv_fp4_halo_kernel<16, 3>}};
+    const KernT kern = kerns[g.nepi == 16][flags];
+    static SmemOptIn attr[2][4];
+    LB_CUDA_TRY(attr[g.nepi == 16][flags].ensure(kern, H7_SMEM));
     const int pairs = prm.ptiles < num_sms() / 2 ? prm.ptiles : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
