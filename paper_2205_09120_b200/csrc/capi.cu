@@ -269,7 +269,8 @@ extern "C" lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, co
     long long rows_per;
     if (staged) {  // ~16 MiB staging slots, whole 256-row m tiles
         const long long row_bytes = a_row_bytes > c_row_bytes ? a_row_bytes : c_row_bytes;
-        rows_per = ((16LL << 20) / row_bytes) / 256 * 256;
+        static const long long slot_mb = lb::tuning_env("LOWBIT_STAGE_MB") ? atoi(lb::tuning_env("LOWBIT_STAGE_MB")) : 16;
+        rows_per = ((slot_mb << 20) / row_bytes) / 256 * 256;
         if (rows_per < 256) rows_per = 256;
         if (rows_per > m) rows_per = m;
         chunks = (int)((m + rows_per - 1) / rows_per);

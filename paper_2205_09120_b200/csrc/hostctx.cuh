@@ -76,8 +76,11 @@ class HostCopier {
     static constexpr size_t kSmallBytes = 256 << 10;
     static int default_threads() {
         const int hw = (int)std::thread::hardware_concurrency();
-        // memcpy pinned -> pageable: 14 GB/s on 1 thread, ~54 GB/s (the PCIe rate) on 8 (host_copy_bw.cu)
-        return hw <= 2 ? 1 : (hw - 1 < 8 ? hw - 1 : 8);
+        // memcpy pinned -> pageable: 14 GB/s on 1 thread, ~54 GB/s (the PCIe rate) on 8 (host_copy_bw.cu);
+        // inside the c5 staging pipeline the host copies bound the call: 76 ms on 8 threads, 71 ms on 15
+        // (tools/e2e_pageable_time.py, 16-CPU box)
+        static const int cap = lb::tuning_env("LOWBIT_COPY_THREADS") ? atoi(lb::tuning_env("LOWBIT_COPY_THREADS")) : 16;
+        return hw <= 2 ? 1 : (hw - 1 < cap ? hw - 1 : cap);
     }
 
   private:
