@@ -58,6 +58,7 @@ CASES = [
     (TNN, False, 2, 9, 9, 128, 64, 3, 1, 1, 0, "HALO_FP4"),
     (TBN, False, 1, 12, 20, 256, 40, 3, 1, 1, 0, "HALO_FP4"),
     (BNN, True, 2, 8, 8, 128, 32, 3, 1, 0, 0, "HALO_FP4"),
+    (BNN, True, 2, 8, 8, 128, 32, 3, 1, 1, 0, "HALO_FP4"),   # padded with binary_pad_value = +1
     (TNN, False, 2, 9, 9, 128, 64, 3, 2, 1, 0, "IMPLICIT_FP4"),
     (BNN, True, 1, 9, 7, 128, 48, 3, 2, 0, 0, "IMPLICIT_FP4"),
     (TNN, False, 2, 9, 9, 128, 64, 3, 1, 1, 4, "IMPLICIT_I8"),
