@@ -624,6 +624,28 @@ def cpp_dropin_e2e(mode, M, N, K, seed, iters=3):
         return {"error": repr(e)}
 
 
+def cpp_dropin_conv(batch, h, w, c, cout, seed, iters=3):
+    """Config 4 as `batch` single-image conv2d_lowbit calls through the C++ drop-in
+    (cpp/bench/dropin_e2e.cpp conv)."""
+    exe = os.path.join(ROOT, "paper_2205_09120_b200", "cpp", "build", "dropin_e2e")
+    if not os.path.exists(exe):
+        return {"unavailable": "cpp/build/dropin_e2e not built"}
+    try:
+        r = subprocess.run([exe, "conv", "1", str(batch), str(h), str(w), str(c), str(cout), str(iters), str(seed)],
+                           capture_output=True, text=True, timeout=600)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not line:
+            return {"error": f"rc={r.returncode} {r.stderr[-300:]}"}
+        d = json.loads(line[-1])
+        return {"ms_64_images": d["ms_median"], "TOPS": d["TOPS"], "equal_device_path": d["equal_device_path"],
+                "path": "C++ drop-in: 64 x lowbit::conv2d_lowbit(tnn, FeatureMap, SignMatrix, ConvSpec) -> "
+                        "IntFeatureMap, host clock (each call uploads its image, runs K7, widens to int32 and "
+                        "downloads; the weights are encoded, packed, uploaded and prepared by the first call "
+                        "and reused while they are unchanged)"}
+    except Exception as e:
+        return {"error": repr(e)}
+
+
 def flush_l2(flush):
     """Evict L2 between timed steps: write a 256 MiB buffer (2x the 126 MB L2),
     then read it back so the lines left in L2 are clean — otherwise the next
@@ -828,6 +850,10 @@ def side_configs(lb, torch, flush, pk):
     k4_bytes = 64 * 56 * 56 * 128 + 2 * 200704 * pitch
     res["k4_encode"] = {"ms": ms, "GB/s": k4_bytes / (ms * 1e-3) / 1e9,
                         "frac_hbm": k4_bytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": k4_bytes}
+    # config 4 through the C++ drop-in exactly as a reference caller runs the batch: 64 single-image
+    # lowbit::conv2d_lowbit(mode, FeatureMap, SignMatrix, ConvSpec) calls (conv.hpp:64-65), host
+    # clock, std::vector in / IntFeatureMap out (weights encoded + packed per call, as conv.cpp:49)
+    res["cpp_dropin"] = cpp_dropin_conv(64, 56, 56, 128, 128, 46)
     out["c4"] = res
     # c5 "from int8 A": the int8 sign matrix straight to the tensor cores (no encode)
     a = lb.generate(0, 47, 0, 1048576, 2048)

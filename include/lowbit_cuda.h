@@ -239,7 +239,10 @@ lowbit_status lowbit_conv2d(int mode, const int8_t* fm, int batch, int h, int w,
                             int padding, int binary_pad_value, void* workspace, int* zero_flag, int16_t* out,
                             int kernel, lowbit_stream stream);
 /* Host-buffer drop-in of conv2d_lowbit: host NHWC fm, host PackedB panels of
- * the (kh*kw*c) x cout weights, host int32 NHWC out (IntFeatureMap). */
+ * the (kh*kw*c) x cout weights, host int32 NHWC out (IntFeatureMap).
+ * The prepared weights of the last call on this thread and device are kept
+ * and reused while the panel bytes (and b_ternary, cout, k) are identical, so
+ * a batch of single-image calls uploads and prepares the weights once. */
 lowbit_status lowbit_conv2d_host(int mode, const int8_t* fm, int batch, int h, int w, int c, int fm_binary,
                                  const uint8_t* panels, int b_ternary, int cout, int k, int kh, int kw, int stride,
                                  int padding, int binary_pad_value, int32_t* out, lowbit_stream stream);

@@ -10,7 +10,10 @@
 // device-resident path (lowbit_gemm on prepared weights).
 //
 //   dropin_e2e MODE M N K ITERS SEED   (MODE 0 bnn, 1 tnn, 2 tbn)
-// prints one JSON object.
+//   dropin_e2e conv MODE BATCH H W C COUT ITERS SEED   (3x3, stride 1, pad 1: config 4's layer)
+// prints one JSON object.  The conv form times BATCH single-image
+//     IntFeatureMap o = lowbit::conv2d_lowbit(mode, fm_i, weights, spec);
+// calls per iteration, as a reference caller runs a batch (conv.hpp:64-65 takes one image).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +24,7 @@
 #include <vector>
 
 #include "../../../include/lowbit_cuda.h"
+#include "lowbit/conv.hpp"
 #include "lowbit/gemm.hpp"
 
 using namespace lowbit;
@@ -60,7 +64,100 @@ static void planes(int dist, unsigned long long seed, int id, int rows, int cols
     cudaFree(flag);
 }
 
+// host int8 values from the device generator (identical to the oracle's)
+static std::vector<std::int8_t> gen_host(int dist, unsigned long long seed, int id, long long rows, long long cols) {
+    int8_t* v;
+    cudaMalloc(&v, (size_t)(rows * cols));
+    CK(lowbit_generate(dist, seed, id, 0, rows, cols, v, nullptr));
+    std::vector<std::int8_t> h((size_t)(rows * cols));
+    cudaMemcpy(h.data(), v, h.size(), cudaMemcpyDeviceToHost);
+    cudaFree(v);
+    return h;
+}
+
+static int conv_main(int argc, char** argv) {
+    if (argc < 10) {
+        std::fprintf(stderr, "usage: dropin_e2e conv MODE BATCH H W C COUT ITERS SEED\n");
+        return 1;
+    }
+    const int mode = std::atoi(argv[2]), batch = std::atoi(argv[3]), h = std::atoi(argv[4]), w = std::atoi(argv[5]);
+    const int c = std::atoi(argv[6]), cout = std::atoi(argv[7]), iters = std::atoi(argv[8]);
+    const unsigned long long seed = std::strtoull(argv[9], nullptr, 10);
+    const bool a_bin = mode == 0, b_ter = mode == 1;
+    const int da = a_bin ? 1 : 0, db = b_ter ? 0 : 1, k = 9 * c;
+    const std::vector<std::int8_t> all = gen_host(da, seed, 0, (long long)batch * h * w, c);
+    std::vector<FeatureMap> fms;
+    for (int i = 0; i < batch; ++i) {
+        FeatureMap f(h, w, c, a_bin ? Mode::binary : Mode::ternary);
+        std::memcpy(f.values.data(), all.data() + (size_t)i * h * w * c, (size_t)h * w * c);
+        fms.push_back(std::move(f));
+    }
+    SignMatrix wt(k, cout, b_ter ? Mode::ternary : Mode::binary);
+    wt.values = gen_host(db, seed, 1, k, cout);
+    ConvSpec spec;
+    spec.kernel_h = spec.kernel_w = 3;
+    spec.stride = 1;
+    spec.padding = 1;
+    spec.out_channels = cout;
+    // check image 0 against the device-resident path (lowbit_conv2d on the same weights)
+    const IntFeatureMap o0 = conv2d_lowbit((GemmMode)mode, fms[0], wt, spec);
+    bool equal = false;
+    {
+        const PackedB pb = b_ter ? pack_b(encode_ternary(wt)) : pack_b(encode_binary(wt));
+        std::vector<std::uint8_t> stream;
+        for (auto& p : pb.panels) stream.insert(stream.end(), p.buffer.begin(), p.buffer.end());
+        uint8_t* pan;
+        void *wts, *ws;
+        int8_t* dfm;
+        int16_t* dout;
+        int* flag;
+        cudaMalloc(&pan, stream.size());
+        cudaMemcpy(pan, stream.data(), stream.size(), cudaMemcpyHostToDevice);
+        cudaMalloc(&wts, lowbit_weights_bytes(b_ter, cout, k));
+        CK(lowbit_prepare_weights(b_ter, pan, cout, k, wts, nullptr));
+        cudaMalloc(&dfm, (size_t)h * w * c);
+        cudaMemcpy(dfm, fms[0].values.data(), (size_t)h * w * c, cudaMemcpyHostToDevice);
+        const size_t wsb = lowbit_conv2d_workspace_bytes(mode, 1, h, w, c, 3, 3, 1, 1);
+        cudaMalloc(&ws, wsb > 256 ? wsb : 256);
+        cudaMalloc(&dout, (size_t)h * w * cout * 2);
+        cudaMalloc(&flag, 4);
+        cudaMemset(flag, 0, 4);
+        CK(lowbit_conv2d(mode, dfm, 1, h, w, c, a_bin ? 1 : 0, wts, b_ter ? 1 : 0, cout, k, 3, 3, 1, 1, 1, ws, flag,
+                         dout, LOWBIT_KERNEL_AUTO, nullptr));
+        std::vector<int16_t> want((size_t)h * w * cout);
+        cudaMemcpy(want.data(), dout, want.size() * 2, cudaMemcpyDeviceToHost);
+        equal = o0.values.size() == want.size();
+        for (size_t i = 0; equal && i < want.size(); ++i) equal = o0.values[i] == (int32_t)want[i];
+        cudaFree(pan);
+        cudaFree(wts);
+        cudaFree(dfm);
+        cudaFree(ws);
+        cudaFree(dout);
+        cudaFree(flag);
+    }
+    std::vector<double> ms;
+    for (int it = 0; it < iters; ++it) {
+        auto t0 = std::chrono::steady_clock::now();
+        long long sum = 0;
+        for (int i = 0; i < batch; ++i) {
+            const IntFeatureMap o = conv2d_lowbit((GemmMode)mode, fms[i], wt, spec);
+            sum += o.values[(size_t)i % o.values.size()];
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+        if (sum == 0x7FFFFFFFFFFFLL) return 5;  // keep the results live
+    }
+    std::sort(ms.begin(), ms.end());
+    const double med = ms[ms.size() / 2];
+    const double ops = 2.0 * batch * h * w * (double)cout * k;
+    std::printf("{\"conv\": true, \"mode\": %d, \"batch\": %d, \"h\": %d, \"w\": %d, \"c\": %d, \"cout\": %d, "
+                "\"iters\": %d, \"ms_median\": %.3f, \"TOPS\": %.3f, \"equal_device_path\": %s}\n",
+                mode, batch, h, w, c, cout, iters, med, ops / (med * 1e-3) / 1e12, equal ? "true" : "false");
+    return equal ? 0 : 4;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && std::strcmp(argv[1], "conv") == 0) return conv_main(argc, argv);
     if (argc < 7) {
         std::fprintf(stderr, "usage: dropin_e2e MODE M N K ITERS SEED\n");
         return 1;

@@ -182,6 +182,11 @@ struct HostCtx {
     DevScratch a0, a1, panels, weights, c, vals, flag;
     // conv2d
     DevScratch fm, ws, out16, out32;
+    // conv2d's prepared weights, kept while successive calls pass the same PackedB (a batch of
+    // single-image conv2d_lowbit calls, conv.hpp:64-65): conv_w_key holds those panel bytes
+    DevScratch conv_w;
+    std::vector<uint8_t> conv_w_key;
+    int conv_w_ternary = -1, conv_w_cout = 0, conv_w_k = 0;
     PinnedScratch bounce_in[kBounce], bounce_out[kBounce];
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_in[kChunks] = {}, ev_c[kChunks] = {}, ev_w = nullptr, ev_done = nullptr;
@@ -213,7 +218,9 @@ struct HostCtx {
         if (prev != dev) cudaSetDevice(dev);
         if (s_in) cudaStreamSynchronize(s_in);
         if (s_out) cudaStreamSynchronize(s_out);
-        for (DevScratch* b : {&a0, &a1, &panels, &weights, &c, &vals, &flag, &fm, &ws, &out16, &out32}) b->release();
+        for (DevScratch* b : {&a0, &a1, &panels, &weights, &c, &vals, &flag, &fm, &ws, &out16, &out32, &conv_w}) b->release();
+        conv_w_key.clear();
+        conv_w_ternary = -1;
         for (int i = 0; i < kBounce; ++i) {
             bounce_in[i].release();
             bounce_out[i].release();
