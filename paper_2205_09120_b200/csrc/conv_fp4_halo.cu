@@ -87,6 +87,15 @@ struct HaloParams {
     int* zero_flag;
 };
 
+// Timing experiments (HaloParams::dbg) exist only in -DLOWBIT_TUNING builds: in the product
+// kernel H7_DBG is the constant 0, so the experiments' branches and constants are compiled out
+// (left in, their hoisted register set-ups cost the epilogue ~90 instructions per tile).
+#ifdef LOWBIT_TUNING
+#define H7_DBG(bits) (prm.dbg & (bits))
+#else
+#define H7_DBG(bits) 0
+#endif
+
 // dbg & 32: per-tile event times (clock64) of pair 0's leader CTA, read by lowbit_debug_halo_trace
 __device__ unsigned long long g_halo_trace[16 * 64];
 // dbg & 32: kernel phases in %globaltimer ns over all CTAs: first entry, last end of setup,
@@ -98,7 +107,7 @@ LB_DEV unsigned long long h7_gtime() {
     return t;
 }
 #define H7_TRACE(ev, i) \
-    if ((prm.dbg & 32) && pair == 0 && leader && (i) < 64) g_halo_trace[(ev) * 64 + (i)] = clock64()
+    if (H7_DBG(32) && pair == 0 && leader && (i) < 64) g_halo_trace[(ev) * 64 + (i)] = clock64()
 
 LB_DEV uint64_t h7_desc_sw64(uint32_t smem_addr) {  // K-major, 64-byte rows, 8-row atoms every 512 B
     uint64_t d = 0;
@@ -141,9 +150,15 @@ LB_DEV bool h7_all_nonzero(uint4 v) {
 
 // waits of the non-issuing roles: suspend-hinted try_wait (dbg & 1024: plain try_wait)
 LB_DEV void h7_wait(int dbg, uint64_t* bar, uint32_t parity) {
+#ifdef LOWBIT_TUNING
     if (dbg & 1024) mbar_wait(bar, parity);
     else mbar_wait_sleep(bar, parity);
+#else
+    (void)dbg;
+    mbar_wait_sleep(bar, parity);
+#endif
 }
+
 
 // FLAGS bit 0 (PADFILL): a binary map padded with +-1 — the converters write the pad codes;
 // bit 1 (CHECKZ): a binary BNN map — a 0 in a real pixel raises ZeroInBinaryInput (core.cpp:23).
@@ -155,9 +170,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                          const HaloParams prm) {
     constexpr int H7_W_CONV = NEPI, H7_W_PROD = H7_W_CONV + H7_NCONV, H7_W_MMA = H7_W_PROD + 1;
     constexpr bool PADFILL = (FLAGS & 1) != 0, CHECKZ = (FLAGS & 2) != 0;
-    if (prm.dbg & 32768) return;  // launch-overhead probe
+    if (H7_DBG(32768)) return;  // launch-overhead probe
 
-    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMin(&g_halo_phase[0], h7_gtime());
+    if (H7_DBG(32) && threadIdx.x == 0) atomicMin(&g_halo_phase[0], h7_gtime());
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int CB = prm.cblocks;
@@ -185,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int bn = prm.bn, bnh = bn >> 1;
-    const int my_tiles = (prm.ptiles > pair && !(prm.dbg & 2048)) ? (prm.ptiles - pair + npairs - 1) / npairs : 0;
+    const int my_tiles = (prm.ptiles > pair && !H7_DBG(2048)) ? (prm.ptiles - pair + npairs - 1) / npairs : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < H7_MAX_ST; ++s) {
@@ -224,7 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     // programmatic dependent launch: the setup above (barriers, TMEM, the k-block table)
     // overlaps the previous kernel's tail; global memory is touched only after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[1], h7_gtime());
+    if (H7_DBG(32) && threadIdx.x == 0) atomicMax(&g_halo_phase[1], h7_gtime());
 
     if (warp == H7_W_PROD) {
         // ===================== TMA producer (both CTAs): filter + raw halos =====================
@@ -241,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     const uint32_t s = t % prm.raw_st;
                     h7_wait(prm.dbg, &raw_empty[s], ((t / prm.raw_st) & 1) ^ 1);
                     if (nt == 0) H7_TRACE(0, i);
-                    if (prm.dbg & 512) {  // timing experiment: no raw loads (stale halo)
+                    if (H7_DBG(512)) {  // timing experiment: no raw loads (stale halo)
                         mbar_arrive(&raw_full[s]);
                         continue;
                     }
@@ -264,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         // every shared-memory store: the stores' asm clobbers memory)
         const int P = prm.P, lp = prm.log2p, rows_h = prm.rows_h, raw_st = prm.raw_st, f4_st = prm.f4_st;
         const int raw_cb = prm.raw_cb, f4_cb = prm.f4_cb, tpi = prm.tpi, R = prm.R, ctiles = prm.ctiles;
-        const bool convert = !(prm.dbg & 4);
+        const bool convert = !H7_DBG(4);
         const int dbg = prm.dbg;
         const int npos = rows_h * P;             // a multiple of 32
         constexpr int STEP = 4 * H7_NCONV;     // positions per iteration of all converter warps
@@ -362,8 +377,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
             const uint32_t breg16 = (uint32_t)prm.breg >> 4;
             const uint64_t bd0 = h7_desc_sw64(smem_u32(sB));
             const uint32_t p4 = (uint32_t)prm.P * 4;  // one halo row of positions in 16-byte units
-            const bool skip_mma = (prm.dbg & 2) != 0;
-            const bool single = (prm.dbg & 4096) != 0;      // timing experiment: one issuer for all tiles
+            const bool skip_mma = H7_DBG(2) != 0;
+            const bool single = H7_DBG(4096) != 0;      // timing experiment: one issuer for all tiles
             mbar_wait(sf_ready, 0);
             tc_fence_after();
             uint32_t t = 0;
@@ -446,14 +461,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 const int ct = (pair + i * npairs) * 2 + (int)rank;
                 const int img = ct / prm.tpi;
                 const int oy = (ct - img * prm.tpi) * prm.R + ry;
-                const bool store_ok = ct < prm.ctiles && oy < prm.oh && !(prm.dbg & 1);
+                const bool store_ok = ct < prm.ctiles && oy < prm.oh && !H7_DBG(1);
                 // one warp of the group waits on the mbarrier, the other seven block on a named
                 // barrier: sixteen wait loops cost issue slots the converters need
-                if (!(prm.dbg & 64) && (warp & 7) == 0) h7_wait(prm.dbg, &tmem_full[acc], acc_phase);
+                if (!H7_DBG(64) && (warp & 7) == 0) h7_wait(prm.dbg, &tmem_full[acc], acc_phase);
                 named_bar_sync(1 + tgrp, 256);
                 tc_fence_after();
                 if (wq == 0 && lane == 0) H7_TRACE(7, u);
-                if (prm.dbg & 128) {  // timing experiment: drain nothing
+                if (H7_DBG(128)) {  // timing experiment: drain nothing
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tmem_empty0 + acc * 8);
@@ -480,33 +495,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 // TMA store: 32 pixels x 64 columns per instruction, clipped at the image's
                 // right / bottom edge by the tensor map.  Direct per-lane 32-byte stores cost 32
                 // L1 lines per instruction and their stalls delayed the accumulator's release.
+                auto load16 = [&](int chunk, uint32_t (&v)[16]) {
+                    if (!H7_DBG(8)) {
+                        tmem_ld_32x32b_x16(tacc + chunk * 16, v);
+                        tmem_ld_wait();
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) v[q] = (uint32_t)q;
+                    }
+                };
                 for (int g = ch0; g < ch1; g += 4) {
                     const int nc = ch1 - g < 4 ? ch1 - g : 4;
+                    const bool last_box = g + 4 >= ch1;
                     if (lane == 0) bulk_wait_read<0>();  // the previous box left the staging buffer
                     __syncwarp();
+                    if (nc == 4) {  // a full box: SW128, 16-byte unit q of row `lane` at ((q ^ (lane & 7)) << 4)
+                        const uint32_t row = stg + lane * 128;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        if (c >= nc) break;
-                        uint32_t v[16], w8[8];
-                        if (!(prm.dbg & 8)) {
-                            tmem_ld_32x32b_x16(tacc + (g + c) * 16, v);
-                            tmem_ld_wait();
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < 16; ++q) v[q] = (uint32_t)q;
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t v[16], w8[8];
+                            load16(g + c, v);
+                            if (c == 3 && last_box) release();
+                            pack16(v, w8);
+                            if (!H7_DBG(16)) {
+                                sts_v4(row + (((2 * c) ^ (lane & 7)) << 4), w8[0], w8[1], w8[2], w8[3]);
+                                sts_v4(row + (((2 * c + 1) ^ (lane & 7)) << 4), w8[4], w8[5], w8[6], w8[7]);
+                            }
                         }
-                        if (c == nc - 1 && g + 4 >= ch1) release();
-                        pack16(v, w8);
-                        if (prm.dbg & 16) {  // timing experiment: no staging stores
-                        } else if (nc == 4) {  // SW128: 16-byte unit q of row `lane` at ((q ^ (lane & 7)) << 4)
-                            const uint32_t row = stg + lane * 128;
-                            sts_v4(row + (((2 * c) ^ (lane & 7)) << 4), w8[0], w8[1], w8[2], w8[3]);
-                            sts_v4(row + (((2 * c + 1) ^ (lane & 7)) << 4), w8[4], w8[5], w8[6], w8[7]);
-                        } else {        // SW32 1 KB boxes
-                            const uint32_t row = stg + c * 1024 + lane * 32;
-                            const uint32_t sw = (uint32_t)(lane >> 2) & 1;
-                            sts_v4(row + (sw << 4), w8[0], w8[1], w8[2], w8[3]);
-                            sts_v4(row + ((sw ^ 1) << 4), w8[4], w8[5], w8[6], w8[7]);
+                    } else {  // a tail of 1-3 chunks: SW32 1 KB boxes
+                        const uint32_t sw = (uint32_t)(lane >> 2) & 1;
+                        for (int c = 0; c < nc; ++c) {
+                            uint32_t v[16], w8[8];
+                            load16(g + c, v);
+                            if (c == nc - 1 && last_box) release();
+                            pack16(v, w8);
+                            if (!H7_DBG(16)) {
+                                const uint32_t row = stg + c * 1024 + lane * 32;
+                                sts_v4(row + (sw << 4), w8[0], w8[1], w8[2], w8[3]);
+                                sts_v4(row + ((sw ^ 1) << 4), w8[4], w8[5], w8[6], w8[7]);
+                            }
                         }
                     }
                     fence_proxy_async_smem();
@@ -529,13 +556,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     // this CTA's work is issued: the next kernel in the stream may begin launching
     // (its griddepcontrol.wait still waits for this grid to complete)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[2], h7_gtime());
+    if (H7_DBG(32) && threadIdx.x == 0) atomicMax(&g_halo_phase[2], h7_gtime());
     cluster_sync();
     if (warp == H7_W_MMA) {
         tc_fence_after();
         tmem_dealloc_pair<512>(tmem_base);
     }
-    if ((prm.dbg & 32) && threadIdx.x == 0) atomicMax(&g_halo_phase[3], h7_gtime());
+    if (H7_DBG(32) && threadIdx.x == 0) atomicMax(&g_halo_phase[3], h7_gtime());
 }
 
 static int h7_pick_bn(int cout) {
