@@ -54,7 +54,7 @@ constexpr int H7_BM = 128;        // output positions per CTA tile (256 per pair
 // alternate tiles, two tiles in flight (5% faster on config 4) — when their 64 KB
 // of staging fits next to the filter and the halo rings, else 8.
 constexpr int H7_NCONV = 8;       // converter warps
-__host__ __device__ constexpr int h7_threads(int nepi) { return 32 * (nepi + H7_NCONV + 3); }
+__host__ __device__ constexpr int h7_threads(int nepi) { return 32 * (nepi + H7_NCONV + 4); }
 constexpr int H7_MAX_BN = 240;    // cout per tile: accumulators + scales <= 512 TMEM columns
 constexpr uint32_t H7_SF_COL = 480;
 constexpr int H7_SMEM = 227 * 1024;
@@ -168,7 +168,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     conv_fp4_halo_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_raw,
                          const __grid_constant__ CUtensorMap tmap_c64, const __grid_constant__ CUtensorMap tmap_c16,
                          const HaloParams prm) {
-    constexpr int H7_W_CONV = NEPI, H7_W_PROD = H7_W_CONV + H7_NCONV, H7_W_MMA = H7_W_PROD + 1;
+    constexpr int H7_W_CONV = NEPI, H7_W_PROD = H7_W_CONV + H7_NCONV, H7_W_MMA = H7_W_PROD + 1,
+                  H7_W_WAIT = H7_W_MMA + 2;
     constexpr bool PADFILL = (FLAGS & 1) != 0, CHECKZ = (FLAGS & 2) != 0;
     if (H7_DBG(32768)) return;  // launch-overhead probe
 
@@ -280,7 +281,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         const int P = prm.P, lp = prm.log2p, rows_h = prm.rows_h, raw_st = prm.raw_st, f4_st = prm.f4_st;
         const int raw_cb = prm.raw_cb, f4_cb = prm.f4_cb, tpi = prm.tpi, R = prm.R, ctiles = prm.ctiles;
         const bool convert = !H7_DBG(4);
-        const int dbg = prm.dbg;
         const int npos = rows_h * P;             // a multiple of 32
         constexpr int STEP = 4 * H7_NCONV;     // positions per iteration of all converter warps
         const int nfull = npos / (8 * STEP), nrem = (npos % (8 * STEP)) / STEP;  // batches of 8 iterations, leftover
@@ -295,13 +295,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         for (int nt = 0; nt < prm.n_tiles; ++nt)
             for (int i = 0; i < my_tiles; ++i, ++t) {
                 const uint32_t rs = t % raw_st, fs = t % f4_st;
-                if (cw == 0) {  // one converter warp waits; the others block on a named barrier
-                    h7_wait(dbg, &raw_full[rs], (t / raw_st) & 1);
-                    if (lane == 0) H7_TRACE(1, t);
-                    h7_wait(dbg, &a_empty[fs], ((t / f4_st) & 1) ^ 1);
-                    if (lane == 0) H7_TRACE(2, t);
-                }
-                named_bar_sync(3, 32 * H7_NCONV);
+                // the waiter warp saw this tile's raw halo land and its fp4 slot free (an mbarrier
+                // try_wait costs the waiting thread ~270 cycles even on a completed phase: two per
+                // tile were on the converters' critical path); one named barrier per raw slot
+                named_bar_sync(3 + rs, 32 * (H7_NCONV + 1));
+                if (cw == 0 && lane == 0) H7_TRACE(2, t);
                 int ytop = 0;  // image row of halo row 0 (binary maps: padding / zero checks)
                 if (PADFILL || CHECKZ) {
                     const int ct = (pair + i * npairs) * 2 + (int)rank;
@@ -364,6 +362,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 }
             }
         if (zero && prm.zero_flag) atomicOr(prm.zero_flag, 1);
+    } else if (warp == H7_W_WAIT) {
+        // ===================== converter waiter (both CTAs) =====================
+        // Waits for tile t's raw halo (raw_full) and its free fp4 slot (a_empty), then
+        // releases the converters through named barrier 3 + t % raw_st.  It cannot run more
+        // than raw_st tiles ahead (raw_full of tile t needs the converters' raw_empty of tile
+        // t - raw_st, arrived after their bar.sync on the same barrier), so each barrier
+        // generation pairs one waiter arrival with one converter pass.
+        const int raw_st = prm.raw_st, f4_st = prm.f4_st;
+        uint32_t t = 0;
+        for (int nt = 0; nt < prm.n_tiles; ++nt)
+            for (int i = 0; i < my_tiles; ++i, ++t) {
+                const uint32_t rs = t % raw_st, fs = t % f4_st;
+                h7_wait(prm.dbg, &raw_full[rs], (t / raw_st) & 1);
+                if (lane == 0) H7_TRACE(1, t);
+                h7_wait(prm.dbg, &a_empty[fs], ((t / f4_st) & 1) ^ 1);
+                __syncwarp();
+                named_bar_arrive(3 + rs, 32 * (H7_NCONV + 1));
+            }
     } else if (warp >= H7_W_MMA) {
         // ===================== UMMA issuers (leader CTA): alternate tiles =====================
         // A waiting issuer thread stalls for ~300 cycles per mbarrier wait while
@@ -397,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     mbar_wait_poll(&a_full[fs], (t / prm.f4_st) & 1);
                     tc_fence_after();
                     if (lane == 0) H7_TRACE(5, t);
-                    if (lane == 0) {
+                    {  // the whole warp issues (one elected lane): operands stay in uniform registers
                         const uint32_t d_tmem = tmem_base + (uint32_t)(a * prm.acc_cols);
                         const uint64_t ad0 = h7_desc_sw64(smem_u32(sF4 + fs * f4_stage));
                         if (prm.k33) {
@@ -406,8 +422,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                                 const uint64_t ad = ad0 + (uint32_t)((kb / 3) * p4 + (kb % 3) * 4);
                                 const uint64_t bd = bd0 + (uint32_t)(kb * breg16);
                                 if (!skip_mma || kb == 0) {
-                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
-                                    umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
+                                    umma_mxf4_pair_warp(d_tmem, ad, bd, idesc, sf, kb != 0);
+                                    umma_mxf4_pair_warp(d_tmem, ad + 2, bd + 2, idesc, sf, 1);
                                 }
                             }
                         } else {
@@ -415,14 +431,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                                 const uint64_t ad = ad0 + kb_aoff[kb];
                                 const uint64_t bd = bd0 + (uint64_t)kb * breg16;
                                 if (!skip_mma || kb == 0) {
-                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
-                                    umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
+                                    umma_mxf4_pair_warp(d_tmem, ad, bd, idesc, sf, kb != 0);
+                                    umma_mxf4_pair_warp(d_tmem, ad + 2, bd + 2, idesc, sf, 1);
                                 }
                             }
                         }
-                        umma_commit_pair(&a_empty[fs], 0x3);
-                        umma_commit_pair(&tmem_full[a], 0x3);
-                        H7_TRACE(6, t);
+                        umma_commit_pair_warp(&a_empty[fs], 0x3);
+                        umma_commit_pair_warp(&tmem_full[a], 0x3);
+                        if (lane == 0) H7_TRACE(6, t);
                     }
                     __syncwarp();
                 }
