@@ -387,28 +387,6 @@ LB_DEV void umma_mxf4_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
         : "memory");
 }
-// The same MMA issued by a converged warp: one elected lane issues it.  With warp-uniform
-// operands ptxas keeps them in uniform registers and emits no per-MMA election loop
-// (the lane-0 form above wraps every MMA in ELECT / R2UR.BROADCAST / BRA.U.ANY).
-LB_DEV void umma_mxf4_pair_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t tmem_sf,
-                                uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sf)
-        : "memory");
-}
-LB_DEV void umma_commit_pair_warp(uint64_t* bar, uint16_t cta_mask) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-            smem_u32(bar)),
-        "h"(cta_mask)
-        : "memory");
-}
 // Instruction descriptor, block-scaled kind::mxf4: E2M1 A/B (format 1),
 // UE8M0 scales (bit 23), K-major, dense K = 64, scale-factor ids 0.
 __host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t m, uint32_t n) {

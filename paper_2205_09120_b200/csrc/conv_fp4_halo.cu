@@ -413,7 +413,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     mbar_wait_poll(&a_full[fs], (t / prm.f4_st) & 1);
                     tc_fence_after();
                     if (lane == 0) H7_TRACE(5, t);
-                    {  // the whole warp issues (one elected lane): operands stay in uniform registers
+                    // lane 0 issues (a converged warp with elect.sync issued fewer instructions per MMA
+                    // but ran c4 4% slower, as it did in K5)
+                    if (lane == 0) {
                         const uint32_t d_tmem = tmem_base + (uint32_t)(a * prm.acc_cols);
                         const uint64_t ad0 = h7_desc_sw64(smem_u32(sF4 + fs * f4_stage));
                         if (prm.k33) {
@@ -422,8 +424,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                                 const uint64_t ad = ad0 + (uint32_t)((kb / 3) * p4 + (kb % 3) * 4);
                                 const uint64_t bd = bd0 + (uint32_t)(kb * breg16);
                                 if (!skip_mma || kb == 0) {
-                                    umma_mxf4_pair_warp(d_tmem, ad, bd, idesc, sf, kb != 0);
-                                    umma_mxf4_pair_warp(d_tmem, ad + 2, bd + 2, idesc, sf, 1);
+                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
+                                    umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
                                 }
                             }
                         } else {
@@ -431,14 +433,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                                 const uint64_t ad = ad0 + kb_aoff[kb];
                                 const uint64_t bd = bd0 + (uint64_t)kb * breg16;
                                 if (!skip_mma || kb == 0) {
-                                    umma_mxf4_pair_warp(d_tmem, ad, bd, idesc, sf, kb != 0);
-                                    umma_mxf4_pair_warp(d_tmem, ad + 2, bd + 2, idesc, sf, 1);
+                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
+                                    umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
                                 }
                             }
                         }
-                        umma_commit_pair_warp(&a_empty[fs], 0x3);
-                        umma_commit_pair_warp(&tmem_full[a], 0x3);
-                        if (lane == 0) H7_TRACE(6, t);
+                        umma_commit_pair(&a_empty[fs], 0x3);
+                        umma_commit_pair(&tmem_full[a], 0x3);
+                        H7_TRACE(6, t);
                     }
                     __syncwarp();
                 }
