@@ -852,7 +852,8 @@ def side_configs(lb, torch, flush, pk):
                         "frac_hbm": k4_bytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": k4_bytes}
     # config 4 through the C++ drop-in exactly as a reference caller runs the batch: 64 single-image
     # lowbit::conv2d_lowbit(mode, FeatureMap, SignMatrix, ConvSpec) calls (conv.hpp:64-65), host
-    # clock, std::vector in / IntFeatureMap out (weights encoded + packed per call, as conv.cpp:49)
+    # clock, std::vector in / IntFeatureMap out (the reference packs the weights per call, conv.cpp:49; the
+    # drop-in encodes, packs and prepares them on the first call and reuses them while they are unchanged)
     res["cpp_dropin"] = cpp_dropin_conv(64, 56, 56, 128, 128, 46)
     out["c4"] = res
     # c5 "from int8 A": the int8 sign matrix straight to the tensor cores (no encode)
