@@ -56,6 +56,21 @@ inline bool make_map_conv_out(CUtensorMap* map, void* base, int batch, int oh, i
     return r == CUDA_SUCCESS;
 }
 
+// The int16 NHWC conv output with boxes of {box_cols channels, box_px pixels, box_rows rows, 1 image}.
+inline bool make_map_conv_out_box(CUtensorMap* map, void* base, int batch, int oh, int ow, int cout, uint32_t box_cols,
+                                  uint32_t box_px, uint32_t box_rows, CUtensorMapSwizzle swz) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)cout, (cuuint64_t)ow, (cuuint64_t)oh, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)cout * 2, (cuuint64_t)ow * cout * 2, (cuuint64_t)oh * ow * cout * 2};
+    cuuint32_t box[4] = {box_cols, box_px, box_rows, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // The NHWC int8 feature map [n, h, w, c] as a 4-D tiled map for boxes of
 // {128 channels, `pixels` pixels of a row, `rows` rows, 1 image}, no swizzle:
 // a box may start left of / above the image and run past its right / bottom
