@@ -645,18 +645,9 @@ bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int
     return batch * tpi < 0x7FFFFFFFLL;
 }
 
-bool conv_ts_applies(int h, int w, int c, int cout, int kh, int kw, int stride, int pad, long long batch);
-lowbit_status launch_conv_ts(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int pad,
-                             int check_zero, int pad_value, const void* weights, int b_ternary, int cout,
-                             int16_t* out, int* zero_flag, cudaStream_t stream);
-
 lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cch, int kh, int kw, int pad,
                                int check_zero, int pad_value, const void* weights, int b_ternary, int cout,
                                int16_t* out, int* zero_flag, cudaStream_t stream) {
-    // cout <= 128 and <= 15 k-blocks: the filter-in-TMEM variant (conv_fp4_ts.cu)
-    if (conv_ts_applies(h, w, cch, cout, kh, kw, 1, pad, batch))
-        return launch_conv_ts(fm, batch, h, w, cch, kh, kw, pad, check_zero, pad_value, weights, b_ternary, cout,
-                              out, zero_flag, stream);
     const HaloGeom g = halo_geom(h, w, cch, cout, kh, kw, 1, pad);
     if (!g.ok) return lbhost::set_error(LOWBIT_INVALID_ARGUMENT, "conv halo kernel: unsupported shape");
     const int oh = h + 2 * pad - kh + 1, ow = w + 2 * pad - kw + 1;
