@@ -258,3 +258,39 @@ def test_conv_halo_binary_padding(lb, port, mode):
         with pytest.raises(lb.ZeroInBinaryInput):
             lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, weights_for(lb, wt, BNN), 3, 3, 1, 1,
                              binary_pad_value=0)
+
+
+@pytest.mark.parametrize("mode", [TNN, TBN])
+def test_conv_halo_large_sums(lb, port, mode):
+    # K7's products are +-0.5 and its f32 sums half-integers: drive them far from 0 (all-ones
+    # maps, filters of one sign with odd-step tails) at the deepest filters K7 takes for this
+    # map (3x3 over 256 channels: k = 2304; 5x5 over 128: k = 3200)
+    for (c, ksz, pad) in ((256, 3, 1), (128, 5, 2)):
+        k = ksz * ksz * c
+        assert lb.conv_select(mode, False, 2, 6, 10, c, 48, ksz, ksz, 1, pad) == lb.CONV_PATH_HALO_FP4
+        fm = np.ones((2, 6, 10, c), np.int8)
+        fm[1, ::2] = -1
+        fm[1, 1::3, 2::4] = 0
+        cols = [np.ones(k, np.int8), -np.ones(k, np.int8)]
+        x = np.ones(k, np.int8)
+        x[k // 2:] = -1
+        x[k // 2::7] = 1
+        cols.append(x)
+        x = np.ones(k, np.int8)
+        x[1::3] = 0 if mode == TNN else 1
+        x[5::64] = -1
+        cols.append(x)
+        rng = np.random.default_rng(c)
+        while len(cols) < 48:
+            p1 = rng.uniform(0.6, 1.0)
+            x = np.where(rng.random(k) < p1, 1, -1).astype(np.int8)
+            if mode == TNN:
+                x[rng.random(k) < 0.1] = 0
+            cols.append(x)
+        wt = np.ascontiguousarray(np.stack(cols, axis=1))
+        got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), False, weights_for(lb, wt, mode), ksz, ksz, 1,
+                               pad).cpu().numpy()
+        for img in range(2):
+            want = port.direct_conv(fm[img], False, wt, ksz, ksz, 1, pad)
+            assert (got[img].astype(np.int32) == want).all(), (mode, c, ksz)
+        assert np.abs(got).max() > 1500
