@@ -672,14 +672,18 @@ def time_device(torch, fn, flush, reps=10):
     return float(np.median(ts))
 
 
-def graph_time(torch, fn, reps=20):
-    """Device time of fn() captured once in a CUDA graph, replayed `reps` times
-    back to back (removes the host/ctypes launch path from the measurement)."""
+def graph_time(torch, fn, reps=20, inner=1):
+    """Device time of fn() captured `inner` times back to back in one CUDA graph,
+    replayed `reps` times (removes the host/ctypes launch path from the
+    measurement), per fn().  With inner = 1 a short fn() is bound by the host's
+    graph-replay rate (~10 us per replay here), not by the GPU; inner > 1
+    amortises that and gives the device time of fn() in a stream of calls."""
     fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        fn()
+        for _ in range(inner):
+            fn()
     g.replay()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -688,7 +692,7 @@ def graph_time(torch, fn, reps=20):
         g.replay()
     e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / reps
+    return s.elapsed_time(e) / reps / inner
 
 
 def graph_time_flushed_avg(torch, fn, flush, reps=10):
@@ -750,7 +754,7 @@ def side_configs(lb, torch, flush, pk):
         res = {}
         for kn, lay, kid, pkind in variants:
             f = lambda: lb.gemm_lowbit(mode, planes[lay], w, (M, N, K), kernel=kid, out=c)
-            ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
+            ms = graph_time(torch, f, reps=10, inner=20) if name == "c1" else time_device(torch, f, flush)
             tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12
             if pkind == "auto":  # the kernel lowbit_select_kernel picks for this shape
                 pkind = "fp4" if lb.select_kernel(mode, M, N, K) == lb.KERNEL_TENSOR else "i8"
@@ -770,11 +774,15 @@ def side_configs(lb, torch, flush, pk):
             lb.gemm_lowbit(mode, pl, w, (M, N, K), out=c)
         for kn, f in (("from_int8_encode_then_auto", enc_gemm),
                       ("from_int8_gemm_i8", lambda: lb.gemm_lowbit_i8(mode, a, w, (M, N, K), out=c))):
-            ms = graph_time(torch, f) if name == "c1" else time_device(torch, f, flush)
+            ms = graph_time(torch, f, reps=10, inner=20) if name == "c1" else time_device(torch, f, flush)
             res[kn] = {"ms": ms, "TOPS": 2.0 * M * N * K / (ms * 1e-3) / 1e12}
+        if name == "c1":  # one call alone: a 1-call graph per replay (bound by the host's replay rate)
+            res["auto_single_graph_replay_ms"] = graph_time(
+                torch, lambda: lb.gemm_lowbit(mode, planes[0], w, (M, N, K), kernel=lb.KERNEL_AUTO, out=c))
         res["from_int8_encode_then_auto"]["path"] = "K1 encode (reference planes) + lowbit_gemm AUTO: two launches"
         res["from_int8_gemm_i8"]["path"] = "lowbit_gemm_i8: int8 A by TMA straight into tcgen05 kind::i8"
-        res["timing"] = "cuda graph replay" if name == "c1" else "events, L2 flushed"
+        res["timing"] = ("device time per call in a CUDA graph of 20 back-to-back calls (launch gaps included)"
+                         if name == "c1" else "events, L2 flushed")
         out[name] = res
     # c2: the 64-shape TBN sweep (one launch per shape), captured as one graph
     aps, ws, cs = [], [], []
@@ -790,11 +798,13 @@ def side_configs(lb, torch, flush, pk):
         def sweep():
             for s, (M, N, K) in enumerate(SWEEP):
                 lb.gemm_lowbit(2, aps[s], ws[s], (M, N, K), kernel=kid, out=cs[s])
-        ms = graph_time(torch, sweep, reps=10)
+        ms = graph_time(torch, sweep, reps=10, inner=4)
         res[kn] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12}
     probs = [(aps[s], ws[s], cs[s]) for s in range(len(SWEEP))]
-    ms = graph_time(torch, lambda: lb.gemm_grouped(2, probs), reps=20)
-    res["grouped_one_launch"] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12}
+    ms = graph_time(torch, lambda: lb.gemm_grouped(2, probs), reps=10, inner=20)
+    ms1 = graph_time(torch, lambda: lb.gemm_grouped(2, probs), reps=20)
+    res["grouped_one_launch"] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12,
+                                 "ms_single_graph_replay": ms1}
     # from int8 A: the 64 encodes (one launch each) + the grouped GeMM launch, one graph
     a8 = [lb.generate(2, 44, 2 * s, M, K) for s, (M, N, K) in enumerate(SWEEP)]
 
@@ -804,10 +814,11 @@ def side_configs(lb, torch, flush, pk):
                                            C.c_void_p(aps[s].plane0.data_ptr()), C.c_void_p(aps[s].plane1.data_ptr()),
                                            aps[s].pitch, None, st), "encode")
         lb.gemm_grouped(2, probs)
-    ms = graph_time(torch, sweep_i8, reps=20)
+    ms = graph_time(torch, sweep_i8, reps=10, inner=10)
     res["from_int8_grouped"] = {"ms_64_shapes": ms, "us_per_shape": ms * 1e3 / 64, "TOPS": ops / (ms * 1e-3) / 1e12,
                                 "path": "64 K1 encodes + one grouped bit-serial launch, one graph"}
-    res["timing"] = "cuda graph (64 launches, or 1 grouped launch), replayed"
+    res["timing"] = ("device time per sweep: a CUDA graph of several back-to-back sweeps (64 launches, or 1 grouped "
+                     "launch), replayed; ms_single_graph_replay: one sweep per graph replay (host replay-rate bound)")
     out["c2"] = res
     # c4: conv 64x56x56x128, 3x3 -> 128, s1 p1 (K4 fused im2col+encode + GeMM)
     fm = lb.generate(0, 46, 0, 64 * 56 * 56, 128).view(64, 56, 56, 128)
@@ -834,11 +845,12 @@ def side_configs(lb, torch, flush, pk):
             res[kn]["frac_hbm"] = c4_bytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]
             res[kn]["algorithmic_bytes"] = c4_bytes
             ms10 = graph_time(torch, lambda: lb.conv2d_lowbit(1, fm, False, w, 3, 3, 1, 1, kernel=kid, out=o,
-                                                              workspace=wsp), reps=20)
+                                                              workspace=wsp), reps=10, inner=10)
             res[kn]["ms_back_to_back"] = ms10
     res["auto"] = "tensor_fp4"
     res["timing"] = ("cuda graph of 10 x (L2 flush, conv) minus one of 10 x (L2 flush), averaged (single short "
-                     "launches are quantised by the event clock); ms_back_to_back: 20 graph replays, warm L2")
+                     "launches are quantised by the event clock); ms_back_to_back: per conv in a graph of 10 back-to-back convs, "
+                     "warm L2")
     # K4 alone (HBM-bound): int8 NHWC in, two bit planes out
     pitch = lb.plane_pitch(1152)
     p0 = wsp[: 200704 * pitch]
