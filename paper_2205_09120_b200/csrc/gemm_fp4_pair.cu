@@ -123,9 +123,21 @@ struct Fp4Params {
 // Role timing for profiling experiments (LOWBIT_DEBUG_FP4 bit 3): cycle
 // counters summed over CTAs, read by lowbit_debug_fp4_stats.
 __device__ unsigned long long g_fp4_stats[16];
+// Timing experiments and role timers exist only in -DLOWBIT_TUNING builds: in the product
+// kernel F4_DBG is the constant 0 and the timers are empty, so their branches, clock reads and
+// hoisted constants are compiled out (as in K7, conv_fp4_halo.cu).
+#ifdef LOWBIT_TUNING
+#define F4_DBG(bits) (prm.debug & (bits))
 #define F4_T0() const long long _t0 = (prm.debug & 8) ? clock64() : 0
 #define F4_ACC(var) \
     if (prm.debug & 8) var += clock64() - _t0
+#else
+#define F4_DBG(bits) 0
+#define F4_T0() \
+    do {        \
+    } while (0)
+#define F4_ACC(var) (void)(var)
+#endif
 
 // One 16-byte chunk (32 elements = one plane word per plane) of packed e2m1:
 // output word q takes bit 4i+q of the plane word into nibble i — one shift +
@@ -302,7 +314,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         continue;
                     }
                     for (int j = 0; j < 2; ++j) {
-                        if (!(prm.debug & 8192))
+                        if (!F4_DBG(8192))
                             tma_load_2d_pair_hint(smem_u32(sB + (2 * st + j) * B_BYTES), &tmap_b, b_full0 + st * 8,
                                                   (kb + j) * 128, brow, b_policy);
                         else
@@ -331,7 +343,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 for (int kb = 0; kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t st = t % F4_B_ST;
                     mbar_wait_sleep(SHARED ? &a_empty[st] : &b_empty[st], ((t / F4_B_ST) & 1) ^ 1);
-                    if ((prm.debug & 64) && (i & 1)) {  // timing experiment: half the B traffic (results invalid)
+                    if (F4_DBG(64) && (i & 1)) {  // timing experiment: half the B traffic (results invalid)
                         if (leader) mbar_arrive(&b_full[st]);
                         continue;
                     }
@@ -429,7 +441,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 }
                 for (int kb = 0; !AR && !g2 && kb < prm.kblocks; ++kb, ++t) {
                     const uint32_t sa = t % F4_A_ST, sb = t % F4_B_ST;
-                    if (!(prm.debug & 16) || t < (uint32_t)F4_B_ST) {  // debug 16: MMA issue rate (no waits)
+                    if (!F4_DBG(16) || t < (uint32_t)F4_B_ST) {  // debug 16: MMA issue rate (no waits)
                         {
                             F4_T0();
                             mbar_wait(&a_ready[sa], (t / F4_A_ST) & 1);
@@ -447,7 +459,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         const uint32_t b_addr = smem_u32(sB + sb * F4_B_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)  // K = 64 per MMA = 32 bytes
-                            if (!(prm.debug & 2))
+                            if (!F4_DBG(2))
                             umma_mxf4_pair(d_tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                            umma_desc_k_sw128(b_addr + kk * 32), idesc, sf, sf, (kb | kk) != 0);
                         umma_commit_pair(&a_empty[sa], pair_mask);
@@ -459,7 +471,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                 __syncwarp();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            if ((prm.debug & 8) && lane == 0) {
+            if (F4_DBG(8) && lane == 0) {
                 atomicAdd(&g_fp4_stats[0], (unsigned long long)w_a);
                 atomicAdd(&g_fp4_stats[1], (unsigned long long)w_b);
                 atomicAdd(&g_fp4_stats[2], (unsigned long long)w_t);
@@ -547,7 +559,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             }
             F4_T0();
             const uint32_t raw = sRaw_u + rs * RAW_SLOT + r * 32;
-            if (prm.debug & 1) goto done;
+            if (F4_DBG(1)) goto done;
             {
             const uint4 p0 = lds_v4(raw + (rsw << 4)), p1 = lds_v4(raw + ((rsw ^ 1) << 4));
             uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0;
@@ -575,7 +587,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             }
             F4_ACC(w_work);
         }
-        if ((prm.debug & 8) && lane == 0) {
+        if (F4_DBG(8) && lane == 0) {
             atomicAdd(&g_fp4_stats[4], (unsigned long long)w_raw);
             atomicAdd(&g_fp4_stats[5], (unsigned long long)w_slot);
             atomicAdd(&g_fp4_stats[6], (unsigned long long)w_work);
@@ -626,7 +638,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             F4_T0();
             tc_fence_after();
             const uint32_t tacc = tmem_base + lane_base + (uint32_t)acc * F4_MAX_BN;
-            const int nch = (prm.debug & 4) ? 0 : bn / 16;
+            const int nch = F4_DBG(4) ? 0 : bn / 16;
             // tail first: the next tile's scales go there (its last chunk waits in registers)
             uint32_t vt[16];
             const bool tail_out = bn > (int)F4_SF_OFF && nch > 0 && sf_owner;
@@ -647,11 +659,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             };
             // Groups of EGRP 16-column chunks: one TMEM wait, one wait for the
             // staging buffers, one proxy fence and one bulk group per group.
-            long long _tg = (prm.debug & 8) ? clock64() : 0;
+            long long _tg = F4_DBG(8) ? clock64() : 0;
             const int cend = nch < ch_hi ? nch : ch_hi;
             for (int g0 = ch_lo; g0 < cend; g0 += EGRP) {
                 uint32_t v[EGRP][16];
-                if (!(prm.debug & 256)) {  // debug 256: timing experiment without the TMEM loads
+                if (!F4_DBG(256)) {  // debug 256: timing experiment without the TMEM loads
 #pragma unroll
                     for (int j = 0; j < EGRP; ++j)
                         if (g0 + j < cend && !(tail_out && g0 + j == nch - 1))
@@ -678,7 +690,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         uint32_t h[8];
                         to_i16(v[j], h);
                         const int col0 = nt * bn + ch * 16;
-                        if (prm.debug & 512) {  // timing experiment: no staging stores
+                        if (F4_DBG(512)) {  // timing experiment: no staging stores
                             if ((h[0] ^ h[3] ^ h[7]) == 0x9E3779B9u && lane == 77) sts_v4(epi, h[0], h[1], h[2], h[3]);
                         } else if (prm.tma_store) {
                             // chunk j of the group's 32-column box: 64-byte rows, TMA SWIZZLE_64B
@@ -701,7 +713,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         }
                     }
                 }
-                if (prm.tma_store && !(prm.debug & 128)) {  // debug 128: timing experiment without the stores
+                if (prm.tma_store && !F4_DBG(128)) {  // debug 128: timing experiment without the stores
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
@@ -711,7 +723,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
                         bulk_commit();
                     }
                 }
-                if (prm.debug & 8) {
+                if (F4_DBG(8)) {
                     const long long now = clock64();
                     if (g0 == ch_lo) w_grp0 += now - _tg;
                     else w_grp1 += now - _tg;
@@ -724,7 +736,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (prm.tma_store && lane == 0) bulk_wait<0>();
-        if ((prm.debug & 8) && lane == 0) {
+        if (F4_DBG(8) && lane == 0) {
             atomicAdd(&g_fp4_stats[8], (unsigned long long)w_ep);
             atomicAdd(&g_fp4_stats[9], (unsigned long long)(clock64() - t_start));
             atomicAdd(&g_fp4_stats[10], (unsigned long long)w_tail);
