@@ -86,19 +86,29 @@ LB_DEV uint64_t umma_desc_k_sw64(uint32_t smem_addr) {
     return d;
 }
 
+// Timing experiments (ConvF4Params::dbg) exist only in -DLOWBIT_TUNING builds: C6_DBG is the
+// constant 0 in the product kernel (as in K5 / K7).
+#ifdef LOWBIT_TUNING
+#define C6_DBG(bits) (prm.dbg & (bits))
+#define C6_DBGV(v, bits) ((v) & (bits))
+#else
+#define C6_DBG(bits) 0
+#define C6_DBGV(v, bits) 0
+#endif
+
 // dbg & 32: per-tile event times of pair 0's leader CTA (clock64), read by lowbit_debug_conv_trace
 __device__ unsigned long long g_conv_trace[16 * 64];
 #define C6_TRACE(ev, i)                                                                  \
-    if ((prm.dbg & 32) && pair == 0 && leader && (i) < 64) g_conv_trace[(ev) * 64 + (i)] = clock64()
+    if (C6_DBG(32) && pair == 0 && leader && (i) < 64) g_conv_trace[(ev) * 64 + (i)] = clock64()
 
 LB_DEV void cwait(int dbg, uint64_t* bar, uint32_t parity) {
-    if (dbg & 16) mbar_wait(bar, parity);
+    if (C6_DBGV(dbg, 16)) mbar_wait(bar, parity);
     else mbar_wait_sleep(bar, parity);
 }
 // the MMA thread's waits: polled (dbg & 128: try_wait)
 LB_DEV void mwait(int dbg, uint64_t* bar, uint32_t parity) {
-    if (dbg & 128) mbar_wait(bar, parity);
-    else if (dbg & 8192) mbar_wait_sleep(bar, parity);
+    if (C6_DBGV(dbg, 128)) mbar_wait(bar, parity);
+    else if (C6_DBGV(dbg, 8192)) mbar_wait_sleep(bar, parity);
     else mbar_wait_poll(bar, parity);
 }
 
@@ -109,7 +119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
     conv_fp4_pair_kernel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_c64,
                          const ConvF4Params prm) {
-    if (prm.dbg & 256) return;  // launch-overhead probe
+    if (C6_DBG(256)) return;  // launch-overhead probe
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int A_ST = prm.a_st;
@@ -164,7 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const bool probe_only = (prm.dbg & 512) != 0;  // setup/teardown probe
+    const bool probe_only = C6_DBG(512) != 0;  // setup/teardown probe
 
     if (probe_only) {
     } else if (warp == C6_W_A) {
@@ -187,7 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                         const uint32_t s = t % A_ST;
                         cwait(prm.dbg, &a_empty[s], ((t / A_ST) & 1) ^ 1);
                         C6_TRACE(5, i);
-                        if (!(prm.dbg & 4))
+                        if (!C6_DBG(4))
                             for (int cb = 0; cb < prm.cblocks; ++cb)
                                 for (int l = 0; l < prm.hloads; ++l)
                                     tma_load_2d_pair(smem_u32(sA + s * a_stage + (cb * prm.hloads + l) * KB_BYTES),
@@ -198,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                             // only a few MMAs queued behind it)
                             const int u = (int)t;
                             cwait(prm.dbg, &tmem_empty[u % prm.nacc], ((uint32_t)(u / prm.nacc) & 1) ^ 1);
-                            mbar_arrive_expect_tx(&a_full[s], (prm.dbg & 4) ? 0u : 2u * a_stage);
+                            mbar_arrive_expect_tx(&a_full[s], C6_DBG(4) ? 0u : 2u * a_stage);
                         }
                         C6_TRACE(6, i);
                         ++t;
@@ -250,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
             const int nkb = prm.kblocks;
             const uint32_t breg = (uint32_t)prm.breg, sB32 = smem_u32(sB), breg16 = breg >> 4;
             const uint64_t bd0 = umma_desc_k_sw64(sB32);
-            const bool skip_mma = (prm.dbg & 2) != 0;
+            const bool skip_mma = C6_DBG(2) != 0;
             const bool k33 = prm.oh_kh == 3 && prm.kw == 3 && prm.cblocks == 1;
             const int wp4 = prm.wp * 4;  // one padded pixel row in 16-byte units
             if (TL) {  // k-block kb -> A start offset in 16-byte descriptor units
@@ -284,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                     const uint32_t d_tmem = tmem_base + (uint32_t)(acc * prm.acc_cols);
                     for (int sg = 0; sg < stages_per_tile; ++sg, ++t) {
                         const uint32_t s = t % A_ST;
-                        if (!(prm.dbg & 4096)) mwait(prm.dbg, &a_full[s], (t / A_ST) & 1);
+                        if (!C6_DBG(4096)) mwait(prm.dbg, &a_full[s], (t / A_ST) & 1);
                         tc_fence_after();
                         C6_TRACE(1, i);
                         if (TL && lane == 0) {  // tap (ky,kx): the halo advanced by ky*wp + kx pixel rows
@@ -384,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                 for (int g = ch0; g < ch1; g += 4) {
                     const int nc = ch1 - g < 4 ? ch1 - g : 4;
                     uint32_t v[4][16];
-                    if (prm.dbg & 8) {
+                    if (C6_DBG(8)) {
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -401,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                     __syncwarp();
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        if (c >= nc || (prm.dbg & 2048)) break;
+                        if (c >= nc || C6_DBG(2048)) break;
                         uint32_t h[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j)  // exact f32 integer -> int16 (see gemm_fp4_pair.cu)
@@ -419,10 +429,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C6_THREADS, 1)
                         }
                     }
                     if ((warp & 3) == 0 && lane == 0 && g == 0) C6_TRACE(10, i);
-                    if (!(prm.dbg & 1024)) fence_proxy_async_smem();
+                    if (!C6_DBG(1024)) fence_proxy_async_smem();
                     __syncwarp();
                     if ((warp & 3) == 0 && lane == 0 && g == 0) C6_TRACE(11, i);
-                    if (lane == 0 && !(prm.dbg & 1)) {
+                    if (lane == 0 && !C6_DBG(1)) {
                         const int col = nt * bn + g * 16;
                         if (TL) {  // (a box wholly outside the output is not issued)
                             if (y0 < prm.oh && img0 < nimg && x0 < prm.ow) {

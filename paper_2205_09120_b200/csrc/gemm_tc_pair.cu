@@ -70,9 +70,20 @@ struct PairParams {
 // Timing breakdown for profiling experiments (LOWBIT_DEBUG_PAIR bit 3):
 // per-role cycle counters summed over all CTAs, read by lowbit_debug_pair_stats.
 __device__ unsigned long long g_pair_stats[16];
-#define PR_T0() const long long _t0 = (prm.debug & 8) ? clock64() : 0
+// Timing experiments and role timers exist only in -DLOWBIT_TUNING builds (compiled out of the
+// product kernel, as in K5 / K7).
+#ifdef LOWBIT_TUNING
+#define PR_DBG(bits) (prm.debug & (bits))
+#define PR_T0() const long long _t0 = PR_DBG(8) ? clock64() : 0
 #define PR_ACC(var) \
-    if (prm.debug & 8) var += clock64() - _t0
+    if PR_DBG(8) var += clock64() - _t0
+#else
+#define PR_DBG(bits) 0
+#define PR_T0() \
+    do {        \
+    } while (0)
+#define PR_ACC(var) (void)(var)
+#endif
 
 template <bool A_TER, int LAYOUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
@@ -251,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 __syncwarp();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            if ((prm.debug & 8) && lane == 0) {
+            if (PR_DBG(8) && lane == 0) {
                 atomicAdd(&g_pair_stats[0], (unsigned long long)w_a);
                 atomicAdd(&g_pair_stats[1], (unsigned long long)w_b);
                 atomicAdd(&g_pair_stats[2], (unsigned long long)w_t);
@@ -312,23 +323,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             }
             PR_T0();
             const uint32_t raw = sRaw_u + rs * 2 * PR_RAW_BYTES;
-            if ((prm.debug & 7) == 0) {
+            if (PR_DBG(7) == 0) {
                 expand_row_layout<A_TER, LAYOUT>(raw, raw + PR_RAW_BYTES, sA_u + st * PR_A_BYTES, r);
-            } else if ((prm.debug & 7) == 2) {  // timing experiment: ALU work without the shared-memory stores
+            } else if (PR_DBG(7) == 2) {  // timing experiment: ALU work without the shared-memory stores
                 expand_row<A_TER, 2>(raw, raw + PR_RAW_BYTES, sA_u + st * PR_A_BYTES, r);
-            } else if ((prm.debug & 7) == 4) {  // timing experiment: only the raw loads
+            } else if (PR_DBG(7) == 4) {  // timing experiment: only the raw loads
                 const uint4 pv = lds_v4(raw + r * 16);
                 const uint4 mv = lds_v4(raw + PR_RAW_BYTES + r * 16);
                 if ((pv.x ^ mv.y ^ pv.z ^ mv.w) == 0x9E3779B9u && r == 1000) sts_v4(sA_u, pv.x, 0, 0, 0);
-            } else if ((prm.debug & 7) == 5) {  // timing experiment: only the ALU work, on register data
+            } else if (PR_DBG(7) == 5) {  // timing experiment: only the ALU work, on register data
                 expand_row_regs<A_TER, LAYOUT>((uint32_t)r * 0x9E3779B9u, (uint32_t)t * 0x7F4A7C15u,
                                                sA_u + st * PR_A_BYTES, r);
-            } else if ((prm.debug & 7) == 3) {  // timing experiment: the stores without the ALU work
+            } else if (PR_DBG(7) == 3) {  // timing experiment: the stores without the ALU work
                 const uint32_t row = sA_u + st * PR_A_BYTES + r * 128;
 #pragma unroll
                 for (int ch = 0; ch < 8; ++ch) sts_v4(row + (ch << 4), ch, ch, ch, ch);
             }
-            if (!(prm.debug & 16)) fence_proxy_async_smem();  // debug 16: timing experiment without the fence
+            if (!PR_DBG(16)) fence_proxy_async_smem();  // debug 16: timing experiment without the fence
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&raw_empty[rs]);
@@ -336,7 +347,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             }
             PR_ACC(w_work);
         }
-        if ((prm.debug & 8) && lane == 0) {
+        if (PR_DBG(8) && lane == 0) {
             atomicAdd(&g_pair_stats[4], (unsigned long long)w_raw);
             atomicAdd(&g_pair_stats[5], (unsigned long long)w_slot);
             atomicAdd(&g_pair_stats[6], (unsigned long long)w_work);
@@ -413,7 +424,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (prm.tma_store && lane == 0) bulk_wait<0>();
-        if ((prm.debug & 8) && lane == 0) {
+        if (PR_DBG(8) && lane == 0) {
             atomicAdd(&g_pair_stats[8], (unsigned long long)w_ep);
             atomicAdd(&g_pair_stats[9], (unsigned long long)(clock64() - t_start));
         }
