@@ -75,6 +75,7 @@ struct HaloParams {
     int raw_st, f4_st;         // ring depths
     int nacc, acc_cols;        // TMEM accumulators and their column stride
     int k33;                   // 3x3 filter over one channel block: the unrolled issue loop
+    uint32_t mul16;            // 16: the converters' multiplier (a register operand keeps their shifts IMADs)
     int check_zero;            // binary map: a 0 activation sets *zero_flag (core.cpp:23)
     uint32_t pad_word;         // binary map padded with +-1 (binary_pad_value, conv.cpp:13): 4 int8 pad values;
                                // 0 when the padding reads as 0 (the TMA's out-of-bounds fill)
@@ -119,29 +120,44 @@ LB_DEV uint64_t h7_desc_sw64(uint32_t smem_addr) {  // K-major, 64-byte rows, 8-
     return d;
 }
 
-// 16 int8 {-1, 0, +1} -> 16 packed e2m1 (8 bytes; channel 2i in the low
-// nibble of byte i) encoding +-1 as +-0.5 (0x1 / 0x9): the code is the int8
-// byte ANDed with 0x09 (0x01 -> 0x1, 0xFF -> 0x9, 0x00 -> 0x0), so the whole
-// conversion is AND, SHF + OR per word and one PRMT per word pair.  The
-// filter stays +-1.0, every product is +-0.5, and the f32 sums are
-// half-integers of magnitude <= 16383.5 (exact); the epilogue doubles them.
-LB_DEV uint32_t h7_pack8(uint32_t x0, uint32_t x1) {
-    const uint32_t c0 = x0 & 0x09090909u, c1 = x1 & 0x09090909u;
-    const uint32_t t0 = c0 | (c0 >> 4), t1 = c1 | (c1 >> 4);  // byte 0 = ch0 | ch1 << 4, byte 2 = ch2 | ch3 << 4
-    return __byte_perm(t0, t1, 0x6420);
+// 8 int8 {-1, 0, +1} (two words) -> 8 packed e2m1 codes encoding +-1 as +-0.5
+// (0x1 / 0x9): the code is the int8 byte ANDed with 0x09 (0x01 -> 0x1,
+// 0xFF -> 0x9, 0x00 -> 0x0).  Byte i of the result pairs channel i of x0 (low
+// nibble) with channel i of x1 (high nibble) — the "conv order" of the
+// prepared filter (layout.cuh) — so the whole conversion is two ANDs and one
+// multiply-add per word pair, no byte permute; the multiply-add (by a
+// register operand, so ptxas keeps it an IMAD) runs on the FMA pipe, next to
+// the ALU pipe the ANDs and the domain check use.  The filter stays +-1.0,
+// every product is +-0.5, and the f32 sums are half-integers of magnitude
+// <= 16383.5 (exact); the epilogue doubles them.
+LB_DEV uint32_t h7_mad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+LB_DEV uint32_t h7_pack8(uint32_t x0, uint32_t x1, uint32_t k16) {
+    return h7_mad(x1 & 0x09090909u, k16, x0 & 0x09090909u);
 }
 // Any int8 value, by SIGN as encode_ternary maps it (core.cpp:40-58: v > 0 -> +1,
 // v < 0 -> -1): the code is the nonzero flag in bit 0 and the sign bit in bit 3.
-// The converters take this path only for a 16-channel chunk that holds a value
-// outside {-1, 0, +1} (out_of_sign_domain: two ops per word on the fast path).
+// The converters take this path only for a batch that holds a value outside
+// {-1, 0, +1}.
 LB_DEV uint32_t h7_code4(uint32_t x) { return (nonzero_msb(x) >> 7) | ((x >> 4) & 0x08080808u); }
-LB_DEV uint32_t h7_pack8_sign(uint32_t x0, uint32_t x1) {
-    const uint32_t c0 = h7_code4(x0), c1 = h7_code4(x1);
-    const uint32_t t0 = c0 | (c0 >> 4), t1 = c1 | (c1 >> 4);
-    return __byte_perm(t0, t1, 0x6420);
+LB_DEV uint32_t h7_pack8_sign(uint32_t x0, uint32_t x1) { return (h7_code4(x1) << 4) | h7_code4(x0); }
+// Domain check of four int8: bits 1..7 of the result are all zero iff every byte is in
+// {-1, 0, +1} (bit 0 of each byte is garbage: the caller masks with 0xFEFEFEFE once per
+// batch).  With y = x << 1 (an IMAD on the FMA pipe), bits 2..7 of x ^ y are zero iff
+// bits 1..7 of the byte are equal (0x00, 0x01, 0xFE, 0xFF), and bit 1 of x & ~y picks out
+// 0xFE: one multiply and one LOP3 per word.
+LB_DEV uint32_t h7_bad4(uint32_t x, uint32_t k2) {
+    const uint32_t y = h7_mad(x, k2, 0u);
+    uint32_t f;  // bit 1 of each byte: x & ~y; the other bits: x ^ y (one LOP3; written as asm so
+                 // the caller's final mask is not folded in, which split it into three)
+    asm("lop3.b32 %0, %1, %2, %3, 0x34;" : "=r"(f) : "r"(x), "r"(y), "r"(0x02020202u));
+    return f;
 }
-LB_DEV uint32_t h7_bad16(uint4 v) {
-    return out_of_sign_domain(v.x) | out_of_sign_domain(v.y) | out_of_sign_domain(v.z) | out_of_sign_domain(v.w);
+LB_DEV uint32_t h7_bad16(uint4 v, uint32_t k2) {
+    return h7_bad4(v.x, k2) | h7_bad4(v.y, k2) | h7_bad4(v.z, k2) | h7_bad4(v.w, k2);
 }
 // all 16 bytes nonzero (a binary map holds no 0, core.cpp:23)
 LB_DEV bool h7_all_nonzero(uint4 v) {
@@ -290,6 +306,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         // SW64: 16-byte unit u of row j at j*64 + ((u ^ ((j >> 1) & 3)) << 4); (j >> 1) & 3 is the
         // same for all of this lane's positions (they step by a multiple of 8)
         const uint32_t swz = ((((uint32_t)chunk >> 1) ^ (((uint32_t)j0 >> 1) & 3u)) << 4) + (chunk & 1) * 8;
+        // multipliers held in registers (from a kernel parameter), so the converters'
+        // shifts stay IMADs on the FMA pipe instead of ALU-pipe shifts
+        const uint32_t k16 = prm.mul16, k2 = k16 >> 3;
         bool zero = false;
         uint32_t t = 0;
         for (int nt = 0; nt < prm.n_tiles; ++nt)
@@ -316,6 +335,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                             uint4 v[8];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) v[q] = lds_v4(src + raw_off(jb + STEP * q));
+                            // The tile's last loads are issued: hand the raw slot back now, not after the
+                            // conversion (an arrive is a release: it is ordered after this warp's loads), so
+                            // the producer's next halo load — ~1,800 cycles from issue to landing with the
+                            // epilogue's TMA stores in the same queue — starts ~1,000 cycles earlier.
+                            if (nrem == 0 && cb == CB - 1 && b == nfull - 1) {
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&raw_empty[rs]);
+                            }
                             if (PADFILL || chk) {
 #pragma unroll
                                 for (int q = 0; q < 8; ++q) {
@@ -329,11 +356,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                             uint32_t bad = 0;
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
-                                sts_v2(dst + (uint32_t)(jb + STEP * q) * 64u, h7_pack8(v[q].x, v[q].y),
-                                       h7_pack8(v[q].z, v[q].w));
-                                bad |= h7_bad16(v[q]);
+                                sts_v2(dst + (uint32_t)(jb + STEP * q) * 64u, h7_pack8(v[q].x, v[q].y, k16),
+                                       h7_pack8(v[q].z, v[q].w, k16));
+                                bad |= h7_bad16(v[q], k2);
                             }
-                            if (bad != 0) {  // a value outside {-1, 0, +1}: rewrite the chunks by sign
+                            if ((bad & 0xFEFEFEFEu) != 0) {  // a value outside {-1, 0, +1}: rewrite the chunks by sign
 #pragma unroll
                                 for (int q = 0; q < 8; ++q)
                                     sts_v2(dst + (uint32_t)(jb + STEP * q) * 64u, h7_pack8_sign(v[q].x, v[q].y),
@@ -357,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 __syncwarp();
                 if (cw == 0 && lane == 0) H7_TRACE(3, t);
                 if (lane == 0) {
-                    mbar_arrive(&raw_empty[rs]);
+                    if (nrem != 0 || nfull == 0 || !convert) mbar_arrive(&raw_empty[rs]);  // else released after the last loads
                     mbar_arrive_cluster(a_full0 + fs * 8);
                 }
             }
@@ -653,7 +680,7 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     const int oh = h + 2 * pad - kh + 1, ow = w + 2 * pad - kw + 1;
     const int k = kh * kw * cch;
     const WeightsLayout L(b_ternary, cout, k);
-    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4;
+    const uint8_t* wfp4 = static_cast<const uint8_t*>(weights) + L.off_fp4c;  // conv order (layout.cuh)
 
     HaloParams prm{};
     prm.batch = batch;
@@ -684,6 +711,7 @@ lowbit_status launch_conv_halo(const int8_t* fm, int batch, int h, int w, int cc
     prm.acc_cols = prm.nacc == 3 ? (int)H7_SF_COL / 3 : H7_MAX_BN;
     prm.k33 = kh == 3 && kw == 3 && prm.cblocks == 1;
     prm.check_zero = check_zero;
+    prm.mul16 = 16;
     prm.pad_word = pad > 0 ? (pad_value > 0 ? 0x01010101u : (pad_value < 0 ? 0xFFFFFFFFu : 0u)) : 0u;
     static const int dbg = lb::tuning_env("LOWBIT_HALO_DEBUG") ? atoi(lb::tuning_env("LOWBIT_HALO_DEBUG")) : 0;
     prm.dbg = dbg;

@@ -199,8 +199,9 @@ __global__ void prepare_i8_kernel(int ternary, const uint8_t* __restrict__ panel
 // positions); +1 -> 0x2, -1 -> 0xA, 0 -> 0x0, zero past k.
 //   out  (canonical): element 2i in the low nibble of byte i.
 //   outr (reference order, layout.cuh): nibble 8q+i holds element 4i+q.
+//   outc (conv order, layout.cuh): nibble i of word q holds element 8q + i/2 + 4*(i%2).
 __global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ panels, int n, int k, int np, int kp4,
-                                   uint8_t* __restrict__ out, uint8_t* __restrict__ outr) {
+                                   uint8_t* __restrict__ out, uint8_t* __restrict__ outr, uint8_t* __restrict__ outc) {
     const int db = (k + 7) / 8;
     const int chunks = kp4 / 32;
     const long long total = (long long)np * chunks;
@@ -208,7 +209,7 @@ __global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ pane
          idx += (long long)gridDim.x * blockDim.x) {
         const int col = (int)(idx / chunks);
         const int ch = (int)(idx - (long long)col * chunks);
-        uint32_t words[4] = {0, 0, 0, 0}, rwords[4] = {0, 0, 0, 0};
+        uint32_t words[4] = {0, 0, 0, 0}, rwords[4] = {0, 0, 0, 0}, cwords[4] = {0, 0, 0, 0};
         if (col < n) {
             uint32_t pw = 0, mw = 0;  // the chunk's 32 plus / minus bits, element e at bit e
 #pragma unroll
@@ -229,20 +230,24 @@ __global__ void prepare_fp4_kernel(int ternary, const uint8_t* __restrict__ pane
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                uint32_t w = 0, wr = 0;
+                uint32_t w = 0, wr = 0, wc = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const int e = 8 * q + i, er = 4 * i + q;
+                    const int e = 8 * q + i, er = 4 * i + q, ec = 8 * q + (i >> 1) + 4 * (i & 1);
                     w |= (((pw >> e) & 1u) ? 0x2u : (((mw >> e) & 1u) ? 0xAu : 0x0u)) << (4 * i);
                     wr |= (((pw >> er) & 1u) ? 0x2u : (((mw >> er) & 1u) ? 0xAu : 0x0u)) << (4 * i);
+                    wc |= (((pw >> ec) & 1u) ? 0x2u : (((mw >> ec) & 1u) ? 0xAu : 0x0u)) << (4 * i);
                 }
                 words[q] = w;
                 rwords[q] = wr;
+                cwords[q] = wc;
             }
         }
         reinterpret_cast<uint4*>(out + (size_t)col * (kp4 / 2))[ch] = make_uint4(words[0], words[1], words[2], words[3]);
         reinterpret_cast<uint4*>(outr + (size_t)col * (kp4 / 2))[ch] =
             make_uint4(rwords[0], rwords[1], rwords[2], rwords[3]);
+        reinterpret_cast<uint4*>(outc + (size_t)col * (kp4 / 2))[ch] =
+            make_uint4(cwords[0], cwords[1], cwords[2], cwords[3]);
     }
 }
 
@@ -344,7 +349,7 @@ extern "C" lowbit_status lowbit_prepare_weights(int ternary, const uint8_t* pane
         ternary, panels, n, k, L.np, L.kp, reinterpret_cast<int8_t*>(base));
     LB_CUDA_TRY(cudaGetLastError());
     prepare_fp4_kernel<<<grid_for((long long)L.np * (L.kp4 / 32), 256), 256, 0, s>>>(
-        ternary, panels, n, k, L.np, L.kp4, base + L.off_fp4, base + L.off_fp4r);
+        ternary, panels, n, k, L.np, L.kp4, base + L.off_fp4, base + L.off_fp4r, base + L.off_fp4c);
     LB_CUDA_TRY(cudaGetLastError());
     prepare_bits_kernel<<<grid_for((long long)L.np * L.kw, 256), 256, 0, s>>>(
         ternary, panels, n, k, L.np, L.kw, reinterpret_cast<uint32_t*>(base + L.off_sign),

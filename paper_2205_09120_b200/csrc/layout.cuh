@@ -22,6 +22,14 @@
 //                     operand with the same one shift + mask per plane as the
 //                     NIBBLES layout, and the MMA's depth sum is unchanged
 //                     (A and B are permuted alike; padding is 0 in both).
+//   [ fp4 section, conv order ]
+//                     the same codes with every 8 depth positions paired
+//                     across their halves: byte i of the 4-byte word holds
+//                     depth elements i (low nibble) and 4+i (high nibble) of
+//                     the word's 8.  K7's converters build that word from two
+//                     int8 words with two ANDs and one multiply-add
+//                     ((x1 & 0x09..) * 16 + (x0 & 0x09..)), with no byte
+//                     permute; the MMA's depth sum is unchanged.
 #pragma once
 #include <cstddef>
 
@@ -33,7 +41,7 @@ struct WeightsLayout {
     int kp;  // int8 row length, multiple of 128 bytes (one UMMA k-block)
     int kw;  // words per column in the bit sections, multiple of 8 (one K2 stage)
     int kp4; // fp4 row length in elements, multiple of 256 (one 128-byte fp4 k-block)
-    size_t off_sign, off_nz, off_fp4, off_fp4r, bytes;
+    size_t off_sign, off_nz, off_fp4, off_fp4r, off_fp4c, bytes;
 
     __host__ __device__ WeightsLayout(int ternary_, int n_, int k_) : ternary(ternary_), n(n_), k(k_) {
         np = (n + 255) / 256 * 256;
@@ -44,7 +52,8 @@ struct WeightsLayout {
         off_nz = off_sign + (size_t)np * kw * 4;
         off_fp4 = (off_nz + (ternary ? (size_t)np * kw * 4 : 0) + 1023) / 1024 * 1024;
         off_fp4r = off_fp4 + (size_t)np * kp4 / 2;
-        bytes = off_fp4r + (size_t)np * kp4 / 2;
+        off_fp4c = off_fp4r + (size_t)np * kp4 / 2;
+        bytes = off_fp4c + (size_t)np * kp4 / 2;
     }
 };
 

@@ -30,9 +30,9 @@ for i in range(14):
 print("epilogue warp 0, cycles after epi:full: ld1 wait, cvt1, ld2 wait, cvt2, transpose, done")
 for i in range(8):
     print(i, [ev[e][i] - ev[7][i] for e in (10, 11, 12, 13, 14, 9)])
-print("converter warp 0: a_empty -> converted, -> fenced")
-for i in range(8):
-    print(i, [ev[15][i] - ev[2][i], ev[3][i] - ev[15][i]])
+print("converter warp 0: start -> first load landed, -> last load landed, -> converted + stored, -> fenced")
+for i in range(13):
+    print(i, [ev[10][i] - ev[2][i], ev[11][i] - ev[10][i], ev[15][i] - ev[11][i], ev[3][i] - ev[15][i]])
 def avg(xs):
     xs = [x for x in xs if x > -10**12]
     return sum(xs) / max(len(xs), 1)
