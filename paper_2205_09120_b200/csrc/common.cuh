@@ -224,6 +224,12 @@ LB_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr));
 }
 // Store one value into 16 consecutive columns of this thread's TMEM lane.
+// 16 columns' LOW 16-bit halves as 8 packed words (word q = column 2q | column 2q+1 << 16)
+LB_DEV void tmem_ld_32x32b_x8_pack16(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
 LB_DEV void tmem_st_32x32b_x16_fill(uint32_t taddr, uint32_t x) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "

@@ -56,7 +56,20 @@ constexpr int H7_BM = 128;        // output positions per CTA tile (256 per pair
 constexpr int H7_NCONV = 8;       // converter warps
 __host__ __device__ constexpr int h7_threads(int nepi) { return 32 * (nepi + H7_NCONV + 4); }
 constexpr int H7_MAX_BN = 240;    // cout per tile: accumulators + scales <= 512 TMEM columns
-constexpr uint32_t H7_SF_COL = 480;
+constexpr uint32_t H7_SF_COL = 480;       // unit UE8M0 scales (8 columns)
+constexpr uint32_t H7_SFBIAS_COL = 488;   // the bias MMA's A scales, 2^16 (8 columns)
+// Bias MMA operands: every A element e2m1 1.0, every B element 1.5.  Uniform bytes, so one 8-row
+// swizzle atom (512 B) stands for every atom of the operand: the descriptors' stride between atoms is 0.
+#ifndef H7_BIAS_FULL
+constexpr int H7_BIAS_A = 512, H7_BIAS_B = 512;
+constexpr uint32_t H7_BIAS_SBO = 0;
+#else
+constexpr int H7_BIAS_A = 8 * 1024, H7_BIAS_B = 8 * 1024;  // 128 / up to 120 rows x 64 B
+constexpr uint32_t H7_BIAS_SBO = 512;
+#endif
+#ifndef H7_NEPI_MAX
+#define H7_NEPI_MAX 16
+#endif
 constexpr int H7_SMEM = 227 * 1024;
 constexpr int H7_BAR_BYTES = 1024;  // barriers + the k-block offset table
 __host__ __device__ constexpr int h7_epi_bytes(int nepi) { return nepi * 4096; }  // one 32 px x 64 col box per warp
@@ -110,11 +123,11 @@ LB_DEV unsigned long long h7_gtime() {
 #define H7_TRACE(ev, i) \
     if (H7_DBG(32) && pair == 0 && leader && (i) < 64) g_halo_trace[(ev) * 64 + (i)] = clock64()
 
-LB_DEV uint64_t h7_desc_sw64(uint32_t smem_addr) {  // K-major, 64-byte rows, 8-row atoms every 512 B
+LB_DEV uint64_t h7_desc_sw64(uint32_t smem_addr, uint32_t sbo = 512) {  // K-major, 64-byte rows, 8-row atoms every sbo B
     uint64_t d = 0;
     d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
     d |= (uint64_t)1u << 16;
-    d |= (uint64_t)(512u >> 4) << 32;
+    d |= (uint64_t)(sbo >> 4) << 32;
     d |= (uint64_t)1u << 46;
     d |= (uint64_t)4u << 61;  // SWIZZLE_64B
     return d;
@@ -198,7 +211,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     uint8_t* sRaw = sB + prm.kblocks * prm.breg;             // raw int8 halo ring
     uint8_t* sF4 = sRaw + prm.raw_st * raw_stage;            // fp4 halo ring (the UMMA A operand)
     uint8_t* sEpi = sF4 + prm.f4_st * f4_stage;             // epilogue staging: 4 KB per epilogue warp
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + h7_epi_bytes(NEPI));
+    uint8_t* sBiasA = sEpi + h7_epi_bytes(NEPI);             // the bias MMA's operands (uniform bytes)
+    uint8_t* sBiasB = sBiasA + H7_BIAS_A;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sBiasB + H7_BIAS_B);
     uint64_t* raw_full = bars;            // local: TMA landed the raw halo
     uint64_t* raw_empty = bars + 4;       // local: the converter warps are done with it
     uint64_t* a_full = bars + 8;          // leader: fp4 halos of both CTAs written (all converter warps)
@@ -235,6 +250,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         mbar_init(sf_ready, 16);
         fence_barrier_init();
     }
+    // The bias MMA (see the issuers): every A element 1.0 (0x22), every B element 1.5 (0x33);
+    // uniform bytes, so the swizzle does not matter.
+    for (int i = threadIdx.x; i < (H7_BIAS_A + H7_BIAS_B) / 16; i += h7_threads(NEPI)) {
+        const uint32_t w = i < H7_BIAS_A / 16 ? 0x22222222u : 0x33333333u;
+        sts_v4(smem_u32(sBiasA) + i * 16, w, w, w, w);
+    }
+    fence_proxy_async_smem();
     if (warp == H7_W_PROD && lane == 0) {
         tma_prefetch_desc(&tmap_raw);
         tma_prefetch_desc(&tmap_b);
@@ -419,6 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
             const int nkb = prm.kblocks;
             const uint32_t breg16 = (uint32_t)prm.breg >> 4;
             const uint64_t bd0 = h7_desc_sw64(smem_u32(sB));
+            const uint64_t bias_ad = h7_desc_sw64(smem_u32(sBiasA), H7_BIAS_SBO), bias_bd = h7_desc_sw64(smem_u32(sBiasB), H7_BIAS_SBO);
+            const uint32_t sf_bias = tmem_base + H7_SFBIAS_COL;
             const uint32_t p4 = (uint32_t)prm.P * 4;  // one halo row of positions in 16-byte units
             const bool skip_mma = H7_DBG(2) != 0;
             const bool single = H7_DBG(4096) != 0;      // timing experiment: one issuer for all tiles
@@ -445,13 +469,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     if (lane == 0) {
                         const uint32_t d_tmem = tmem_base + (uint32_t)(a * prm.acc_cols);
                         const uint64_t ad0 = h7_desc_sw64(smem_u32(sF4 + fs * f4_stage));
+                        // The bias MMA sets every accumulator element to 64 * (1.0 * 2^16) * 1.5 = 1.5 * 2^22.
+                        // The taps then add half-integers of magnitude <= 16383.5: every partial sum stays in
+                        // [2^22, 2^23), where the f32 spacing is 0.5 — exact — and the low 16 bits of the
+                        // f32's mantissa are the int16 result (2 * sum mod 2^16), so the epilogue has no
+                        // arithmetic left (tcgen05.ld.pack::16b takes those halves).
+                        if (!H7_DBG(8192)) umma_mxf4_pair(d_tmem, bias_ad, bias_bd, idesc, sf_bias, sf, 0);
                         if (prm.k33) {
 #pragma unroll
                             for (int kb = 0; kb < 9; ++kb) {
                                 const uint64_t ad = ad0 + (uint32_t)((kb / 3) * p4 + (kb % 3) * 4);
                                 const uint64_t bd = bd0 + (uint32_t)(kb * breg16);
-                                if (!skip_mma || kb == 0) {
-                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
+                                if (!skip_mma) {
+                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0 || !H7_DBG(8192));
                                     umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
                                 }
                             }
@@ -459,8 +489,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                             for (int kb = 0; kb < nkb; ++kb) {
                                 const uint64_t ad = ad0 + kb_aoff[kb];
                                 const uint64_t bd = bd0 + (uint64_t)kb * breg16;
-                                if (!skip_mma || kb == 0) {
-                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0);
+                                if (!skip_mma) {
+                                    umma_mxf4_pair(d_tmem, ad, bd, idesc, sf, sf, kb != 0 || !H7_DBG(8192));
                                     umma_mxf4_pair(d_tmem, ad + 2, bd + 2, idesc, sf, sf, 1);
                                 }
                             }
@@ -485,6 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         if (warp < 8) {  // unit UE8M0 scales (sf_ready counts 8 warps x 2 CTAs)
             tmem_st_32x32b_x8_fill(tmem_base + lane_base + H7_SF_COL, 0x7F7F7F7Fu);
+            tmem_st_32x32b_x8_fill(tmem_base + lane_base + H7_SFBIAS_COL, 0x8F8F8F8Fu);  // 2^16: the bias MMA's A scales
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -520,15 +551,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     continue;
                 }
                 const uint32_t tacc = tmem_base + lane_base + (uint32_t)(acc * prm.acc_cols);
-                // f32 sums are half-integers: 2x + 1.5*2^23 is exact and its low 16 bits are the
-                // int16 result (see gemm_fp4_pair.cu); 16 columns -> 8 packed words
-                auto pack16 = [](const uint32_t (&v)[16], uint32_t (&w8)[8]) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        w8[q] = __byte_perm(__float_as_uint(fmaf(__uint_as_float(v[2 * q]), 2.0f, 12582912.0f)),
-                                            __float_as_uint(fmaf(__uint_as_float(v[2 * q + 1]), 2.0f, 12582912.0f)),
-                                            0x5410);
-                };
                 auto release = [&]() {  // the tile's last TMEM read is done: hand the accumulator back
                     tc_fence_before();
                     __syncwarp();
@@ -540,13 +562,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 // TMA store: 32 pixels x 64 columns per instruction, clipped at the image's
                 // right / bottom edge by the tensor map.  Direct per-lane 32-byte stores cost 32
                 // L1 lines per instruction and their stalls delayed the accumulator's release.
-                auto load16 = [&](int chunk, uint32_t (&v)[16]) {
+                // the accumulator holds 1.5 * 2^22 + sum (see the bias MMA): the low 16 bits of each
+                // f32 are the int16 result, and pack::16b loads 16 columns as 8 packed words
+                auto load16 = [&](int chunk, uint32_t (&w8)[8]) {
                     if (!H7_DBG(8)) {
-                        tmem_ld_32x32b_x16(tacc + chunk * 16, v);
-                        tmem_ld_wait();
+                        tmem_ld_32x32b_x8_pack16(tacc + chunk * 16, w8);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) v[q] = (uint32_t)q;
+                        for (int q = 0; q < 8; ++q) w8[q] = (uint32_t)q;
                     }
                 };
                 for (int g = ch0; g < ch1; g += 4) {
@@ -556,24 +579,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     __syncwarp();
                     if (nc == 4) {  // a full box: SW128, 16-byte unit q of row `lane` at ((q ^ (lane & 7)) << 4)
                         const uint32_t row = stg + lane * 128;
+                        uint32_t w[4][8];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            uint32_t v[16], w8[8];
-                            load16(g + c, v);
-                            if (c == 3 && last_box) release();
-                            pack16(v, w8);
-                            if (!H7_DBG(16)) {
-                                sts_v4(row + (((2 * c) ^ (lane & 7)) << 4), w8[0], w8[1], w8[2], w8[3]);
-                                sts_v4(row + (((2 * c + 1) ^ (lane & 7)) << 4), w8[4], w8[5], w8[6], w8[7]);
+                        for (int c = 0; c < 4; ++c) load16(g + c, w[c]);
+                        tmem_ld_wait();
+                        if (last_box) release();
+                        if (!H7_DBG(16)) {
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                sts_v4(row + (((2 * c) ^ (lane & 7)) << 4), w[c][0], w[c][1], w[c][2], w[c][3]);
+                                sts_v4(row + (((2 * c + 1) ^ (lane & 7)) << 4), w[c][4], w[c][5], w[c][6], w[c][7]);
                             }
                         }
                     } else {  // a tail of 1-3 chunks: SW32 1 KB boxes
                         const uint32_t sw = (uint32_t)(lane >> 2) & 1;
                         for (int c = 0; c < nc; ++c) {
-                            uint32_t v[16], w8[8];
-                            load16(g + c, v);
+                            uint32_t w8[8];
+                            load16(g + c, w8);
+                            tmem_ld_wait();
                             if (c == nc - 1 && last_box) release();
-                            pack16(v, w8);
                             if (!H7_DBG(16)) {
                                 const uint32_t row = stg + c * 1024 + lane * 32;
                                 sts_v4(row + (sw << 4), w8[0], w8[1], w8[2], w8[3]);
@@ -641,9 +665,9 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
     // 16 epilogue warps when their staging fits, else 8; ring depths: fp4 3 (2 if tight),
     // raw whatever is left (<= 4, >= 2)
     static const int f4_max = lb::tuning_env("LOWBIT_HALO_F4ST") ? atoi(lb::tuning_env("LOWBIT_HALO_F4ST")) : 3;  // tuning knob
-    static const int nepi_max = lb::tuning_env("LOWBIT_HALO_NEPI8") ? 8 : 16;                            // tuning knob
+    static const int nepi_max = lb::tuning_env("LOWBIT_HALO_NEPI8") ? 8 : H7_NEPI_MAX;                            // tuning knob
     for (int nepi = nepi_max; nepi >= 8; nepi -= 8) {
-        const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - h7_epi_bytes(nepi) - g.kblocks * g.breg;
+        const int budget = H7_SMEM - 1024 - H7_BAR_BYTES - H7_BIAS_A - H7_BIAS_B - h7_epi_bytes(nepi) - g.kblocks * g.breg;
         for (int f4 = f4_max; f4 >= 2; --f4) {
             const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
             if (raw >= 2) {
