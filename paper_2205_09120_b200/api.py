@@ -214,11 +214,14 @@ def conv2d_lowbit(mode: int, fm: torch.Tensor, fm_binary: bool, weights: Weights
     if workspace is None:
         nbytes = int(L.lib.lowbit_conv2d_workspace_bytes(mode, b, h, w, c, kh, kw, stride, padding))
         workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=fm.device)
-    flag = torch.zeros(1, dtype=torch.int32, device=fm.device)
+    # only a BNN conv checks its map for zeros (core.cpp:23); the flag is optional in the C ABI, and
+    # zeroing one per call would put a second kernel launch in front of every ternary conv
+    flag = torch.zeros(1, dtype=torch.int32, device=fm.device) if mode == BNN else None
     L.check(L.lib.lowbit_conv2d(mode, _ptr(fm), b, h, w, c, int(fm_binary), _ptr(weights.buf), int(weights.ternary),
                                 cout, weights.k, kh, kw, stride, padding, binary_pad_value, _ptr(workspace),
-                                _ptr(flag), _ptr(out), kernel, _stream()), "conv2d_lowbit")
-    if mode == BNN and int(flag.item()):
+                                _ptr(flag) if flag is not None else None, _ptr(out), kernel, _stream()),
+            "conv2d_lowbit")
+    if flag is not None and int(flag.item()):
         raise L.ZeroInBinaryInput("binary matrix contains a zero element")
     return out
 

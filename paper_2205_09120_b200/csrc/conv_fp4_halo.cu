@@ -67,6 +67,9 @@ constexpr uint32_t H7_BIAS_SBO = 0;
 constexpr int H7_BIAS_A = 8 * 1024, H7_BIAS_B = 8 * 1024;  // 128 / up to 120 rows x 64 B
 constexpr uint32_t H7_BIAS_SBO = 512;
 #endif
+#ifndef H7_RAW_CAP
+#define H7_RAW_CAP 4
+#endif
 #ifndef H7_NEPI_MAX
 #define H7_NEPI_MAX 16
 #endif
@@ -277,6 +280,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
     const uint32_t tmem_base = *tmem_slot;
     // programmatic dependent launch: the setup above (barriers, TMEM, the k-block table)
     // overlaps the previous kernel's tail; global memory is touched only after this
+    // The next kernel in the stream may begin launching now: its CTAs take each SM as this grid's
+    // CTA leaves it and run their own setup, then block in griddepcontrol.wait until this grid has
+    // completed (c4 back to back: 20.2 -> 19.9 us).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (H7_DBG(32) && threadIdx.x == 0) atomicMax(&g_halo_phase[1], h7_gtime());
 
@@ -285,18 +292,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
         if (lane == 0 && my_tiles > 0) {
             const uint32_t b_full0 = mapa_shared(smem_u32(b_full), 0);
             uint32_t t = 0;
-            for (int nt = 0; nt < prm.n_tiles; ++nt) {
+            auto load_filter = [&](int nt) {
                 h7_wait(prm.dbg, b_empty, (nt & 1) ^ 1);
                 if (leader) mbar_arrive_expect_tx(b_full, (uint32_t)prm.kblocks * bn * 64);
                 const int brow = nt * bn + (int)rank * bnh;
                 for (int kb = 0; kb < prm.kblocks; ++kb)
                     tma_load_2d_pair(smem_u32(sB + kb * prm.breg), &tmap_b, b_full0, kb * 64, brow);
+            };
+            for (int nt = 0; nt < prm.n_tiles; ++nt) {
+                // the kernel's first halo comes from HBM and gates the first tile: it goes out before
+                // the filter (an L2 hit for all but the first CTAs)
+                if (nt > 0) load_filter(nt);
                 for (int i = 0; i < my_tiles; ++i, ++t) {
                     const uint32_t s = t % prm.raw_st;
                     h7_wait(prm.dbg, &raw_empty[s], ((t / prm.raw_st) & 1) ^ 1);
                     if (nt == 0) H7_TRACE(0, i);
                     if (H7_DBG(512)) {  // timing experiment: no raw loads (stale halo)
                         mbar_arrive(&raw_full[s]);
+                        if (t == 0) load_filter(0);
                         continue;
                     }
                     mbar_arrive_expect_tx(&raw_full[s], (uint32_t)raw_stage);
@@ -307,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                     for (int cb = 0; cb < CB; ++cb)
                         tma_load_4d(smem_u32(sRaw + s * raw_stage + cb * prm.raw_cb), &tmap_raw,
                                     smem_u32(&raw_full[s]), cb * 128, -prm.pad, y0 - prm.pad, img);
+                    if (t == 0) load_filter(0);
                 }
             }
         }
@@ -617,14 +631,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(h7_threads(NEPI), 1)
                 }
                 if (wq == 0 && lane == 0) H7_TRACE(9, u);
             }
-        if (lane == 0) bulk_wait<0>();
+        // the staging buffers must outlive the stores' reads; their writes are complete when the grid is
+        if (lane == 0) bulk_wait_read<0>();
     }
 
     tc_fence_before();
     __syncthreads();
-    // this CTA's work is issued: the next kernel in the stream may begin launching
-    // (its griddepcontrol.wait still waits for this grid to complete)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (H7_DBG(32) && threadIdx.x == 0) atomicMax(&g_halo_phase[2], h7_gtime());
     cluster_sync();
     if (warp == H7_W_MMA) {
@@ -672,7 +684,7 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
             const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
             if (raw >= 2) {
                 g.f4_st = f4;
-                static const int raw_max = lb::tuning_env("LOWBIT_HALO_RAWST") ? atoi(lb::tuning_env("LOWBIT_HALO_RAWST")) : H7_MAX_ST;
+                static const int raw_max = lb::tuning_env("LOWBIT_HALO_RAWST") ? atoi(lb::tuning_env("LOWBIT_HALO_RAWST")) : H7_RAW_CAP;
                 g.raw_st = raw < raw_max ? raw : raw_max;  // (tuning knob: LOWBIT_HALO_RAWST caps the raw ring)
                 g.nepi = nepi;
                 g.ok = true;
