@@ -104,8 +104,8 @@ def test_conv_select_paths():
     # stride 2: the fp4 implicit GeMM with a workspace, else the int8 one
     assert sel(L.TNN, False, 3, 8, 7, 128, 96, 3, 3, 2, 1) == lb.CONV_PATH_IMPLICIT_FP4
     assert sel(L.TNN, False, 3, 8, 7, 128, 96, 3, 3, 2, 1, has_workspace=False) == lb.CONV_PATH_IMPLICIT_I8
-    # padded row wider than 128 pixels: K6
-    assert sel(L.TNN, False, 1, 2, 130, 128, 24, 3, 3, 1, 1) == lb.CONV_PATH_IMPLICIT_FP4
+    # padded row wider than 128 pixels: K7 cuts the rows into column blocks
+    assert sel(L.TNN, False, 1, 2, 130, 128, 24, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4
     # a binary map padded with +-1: K7 writes the pad codes (stride 2: K6 / int8 im2col cannot, K4 does);
     # c not a multiple of 128: K4 encode + GeMM
     assert sel(L.BNN, True, 64, 56, 56, 128, 128, 3, 3, 1, 1) == lb.CONV_PATH_HALO_FP4

@@ -194,6 +194,39 @@ def test_conv_halo_geometries(lb, port, mode):
             assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, ch, cout, ksz, pad, img)
 
 
+@pytest.mark.parametrize("mode", [BNN, TNN, TBN])
+def test_conv_halo_column_blocks(lb, port, mode):
+    """K7 with rows cut into column blocks of 32 positions (4 output rows per tile, 32 - (kw - 1)
+    valid outputs per block): chosen when it takes no more tiles than whole rows (config 4's
+    56 x 56 map) and for rows wider than 128 pixels.  Widths that end inside a block, heights not
+    a multiple of 4, two channel blocks, several n tiles, 3x3 / 5x5 / 1x1 filters, padding 0-2;
+    binary maps with every pad value (the converters write the pad codes at each block's edges)
+    and a 0 in a binary map's last block (ZeroInBinaryInput)."""
+    da, db = mode_dists(mode)
+    cases = [(2, 56, 56, 128, 128, 3, 1), (1, 8, 130, 128, 24, 3, 1), (2, 12, 70, 256, 40, 3, 1),
+             (1, 6, 200, 128, 64, 5, 2), (3, 9, 45, 128, 64, 3, 0), (1, 4, 300, 128, 496, 1, 0),
+             (5, 7, 61, 128, 32, 3, 1)]
+    for i, (b, h, w, ch, cout, ksz, pad) in enumerate(cases):
+        binary = mode == BNN
+        assert lb.conv_select(mode, binary, b, h, w, ch, cout, ksz, ksz, 1, pad) == lb.CONV_PATH_HALO_FP4, \
+            (b, h, w, ch, cout, ksz, pad)
+        fm = port.generate(da, 230 + i, 0, b * h * w, ch).reshape(b, h, w, ch)
+        wt = port.generate(db, 230 + i, 1, ksz * ksz * ch, cout)
+        wts = weights_for(lb, wt, mode)
+        for pv in ((1, -1) if binary and pad else (1,)):
+            got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), binary, wts, ksz, ksz, 1, pad,
+                                   binary_pad_value=pv).cpu().numpy()
+            for img in range(b):
+                want = port.direct_conv(fm[img], binary, wt, ksz, ksz, 1, pad, pv)
+                assert (got[img].astype(np.int32) == want).all(), (mode, pv, b, h, w, ch, cout, ksz, pad, img)
+    if mode == BNN:
+        fm = port.generate(1, 239, 0, 2 * 8 * 70, 128).reshape(2, 8, 70, 128)
+        wt = port.generate(1, 239, 1, 9 * 128, 64)
+        fm[1, 7, 69, 100] = 0  # the last pixel of the last block
+        with pytest.raises(lb.ZeroInBinaryInput):
+            lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, weights_for(lb, wt, BNN), 3, 3, 1, 1)
+
+
 @pytest.mark.parametrize("ch", [32, 40])
 def test_conv_binary_zero_only_where_sampled(lb, port, ch):
     """ZeroInBinaryInput follows im2col's view (conv.cpp:9-31, core.cpp:23): a 0 in a
