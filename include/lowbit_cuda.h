@@ -214,7 +214,7 @@ lowbit_status lowbit_gemm_lowbit_host(int mode, const uint8_t* a0, const uint8_t
  * Convs whose padding reads as 0 (ternary maps, or no padding) and whose c
  * is a multiple of 128 run on the tensor cores straight from the int8 map
  * (values in {-1,0,+1}, the FeatureMap contract): K7, a fused halo
- * convolution (stride 1, padded rows of <= 128 pixels), else K6 (fp4
+ * convolution (stride 1, any map width), else K6 (fp4
  * implicit GeMM, uses the workspace), else an int8 implicit GeMM;
  * lowbit_conv_select names the path.  Other convs go through
  * lowbit_conv_encode. */

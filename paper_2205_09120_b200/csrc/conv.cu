@@ -416,7 +416,7 @@ extern "C" size_t lowbit_conv2d_workspace_bytes(int mode, int batch, int h, int 
 }
 
 // Which conv kernel lowbit_conv2d runs (pointers assumed aligned; host logic only):
-//   K7 fused halo conv — stride 1, the padded row fits 128 pixels, c % 128 == 0, the filter + two
+//   K7 fused halo conv — stride 1, any width (column blocks past 128 padded pixels), c % 128 == 0, the filter + two
 //      halo stages fit in shared memory; any padding (binary maps padded with +-1 get the pad
 //      codes written by the converters; a BNN map padded with 0 must raise ZeroInBinaryInput and
 //      takes K4, decided in lowbit_conv2d where the pad value is known);
