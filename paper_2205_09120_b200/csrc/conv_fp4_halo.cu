@@ -10,10 +10,12 @@
 //     image (position i = ry*P + ox).  Its input "halo" is the R + kh - 1
 //     padded input rows starting at y0 - pad, P pixels each starting at
 //     x = -pad: ONE 4-D TMA box of the int8 NHWC map per 128-channel block,
-//     whose out-of-image elements read as zero — the padding.
-//   * Converter warps turn the int8 halo into packed e2m1 (+1 -> 0x2,
-//     -1 -> 0xA, 0 -> 0x0, two channels per byte) in a 64-byte-swizzled
-//     shared-memory tile: halo position j is UMMA row j.
+//     whose out-of-image elements read as zero — the padding.  Rows wider
+//     than 128 padded pixels (or whenever it takes fewer tiles) are cut into
+//     column blocks of P = 32 positions with 32 - (kw - 1) valid outputs.
+//   * Converter warps turn the int8 halo into packed e2m1 (two channels per
+//     byte) in a 64-byte-swizzled shared-memory tile: halo position j is
+//     UMMA row j.
 //   * Filter tap (ky, kx) of output position i reads halo position
 //     i + ky*P + kx, so the A operand of that tap is the halo tile's UMMA
 //     descriptor advanced by ky*P + kx rows (the swizzle is a function of
@@ -23,16 +25,19 @@
 //     never stored).
 //   * The filter (prepared weights, fp4 section, K-major) stays resident in
 //     shared memory; tcgen05.mma.cta_group::2.kind::mxf4.block_scale with
-//     unit scales and f32 accumulators (exact: |partial sums| <= k <= 32767).
-//   * The epilogue: 8 warps, two per TMEM lane quarter, each draining half of
-//     every tile's columns; it reads its whole share of the accumulator
-//     (releasing it to the MMAs at once), converts to int16 into a 128-byte-
-//     swizzled staging box and TMA-stores 32 pixels x 64 columns, clipped at
-//     the image edges by the tensor map.
+//     f32 accumulators.
 //   * Encoding: +-1 activations become +-0.5 (e2m1 0x1 / 0x9 = the int8 byte
 //     AND 0x09; a chunk holding any value outside {-1, 0, +1} is mapped by
-//     sign, as encode_ternary does), the filter stays +-1.0, and the epilogue
-//     doubles the exact half-integer sums.
+//     sign, as encode_ternary does), the filter stays +-1.0: every product is
+//     +-0.5.  A bias MMA first sets every accumulator element to 1.5 * 2^22
+//     (uniform operands under a 2^16 block scale), so the exact partial sums
+//     live in [2^22, 2^23) — f32 spacing 0.5 — and the low 16 bits of each
+//     f32 are the int16 result.
+//   * The epilogue: two warps per TMEM lane quarter and tile, each half of the
+//     tile's columns; tcgen05.ld.pack::16b loads those low halves as packed
+//     words (releasing the accumulator at once), which go into a 128-byte-
+//     swizzled staging box and out by TMA store: 32 pixels x 64 columns,
+//     clipped at the image edges by the tensor map.
 //
 // Warp roles per CTA (NEPI = 16: 864 threads, or 8: 608): 0 .. NEPI-1
 // epilogue (two warps per TMEM lane quarter and tile, each half of the tile's
@@ -780,9 +785,9 @@ HaloGeom halo_geom(int h, int w, int c, int cout, int kh, int kw, int stride, in
 }
 }  // namespace
 
-// Whether K7 takes a conv: stride 1, padding that reads as 0 (ternary map or
-// no padding), 128-channel blocks, a padded row of <= 128 pixels, and a
-// filter + two raw and two fp4 halo stages that fit in shared memory.
+// Whether K7 takes a conv: stride 1, 128-channel blocks, any map width (column
+// blocks past 128 padded pixels), and a filter + two raw and two fp4 halo
+// stages that fit in shared memory.
 bool conv_halo_applies(int fm_binary, int h, int w, int c, int cout, int kh, int kw, int stride, int pad,
                        long long batch) {
     (void)fm_binary;  // binary maps padded with +-1: the converters write the pad codes
