@@ -155,8 +155,9 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     uint64_t* a_empty = bars + 12;      // the tile's MMAs are done with the fp4 halo
     uint64_t* tmem_full = bars + 16;    // (2) accumulator complete
     uint64_t* tmem_empty = bars + 18;   // (2) drained by the 8 epilogue warps of its group
-    uint64_t* f_ready = bars + 20;      // filter, bias operand and scales in TMEM (the 16 epilogue warps)
-    uint64_t* f_tma = bars + 21;        // the filter's TMA boxes landed in the bounce buffers (one phase per round)
+    uint64_t* f_ready = bars + 32;      // (3) a third of the filter's k-blocks is in TMEM (the 16 epilogue warps);
+                                        //     the first also covers the bias operand and the scales
+    uint64_t* f_tma = bars + 35;        // (3) that third's TMA boxes landed in the bounce buffers
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
     uint32_t* kb_boff = reinterpret_cast<uint32_t*>(bars + 24);  // k-block -> halo row offset (16-byte units)
 
@@ -176,8 +177,10 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 8);
         }
-        mbar_init(f_ready, T7_NEPI);
-        mbar_init(f_tma, 1);
+        for (int g = 0; g < 3; ++g) {
+            mbar_init(&f_ready[g], T7_NEPI);
+            mbar_init(&f_tma[g], 1);
+        }
         fence_barrier_init();
     }
     if (threadIdx.x < T7_BIAS_B / 16)  // every B element of the bias MMA is e2m1 1.5
@@ -205,9 +208,29 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (T7_DBG(32) && threadIdx.x == 0) atomicMax(&g_ts_phase[1], t7_gtime());
 
+    // The filter's way into TMEM: TMA brings each k-block's 128 rows x 64 B into a bounce buffer — the
+    // still idle staging boxes, then the last fp4 slot — and the epilogue warps move it on (below).  It
+    // travels in three groups of k-blocks, each with its own barriers, so the first tile's MMAs start
+    // on the first third while the rest is still on its way (148 CTAs pull 136 KB each at once).
+    auto fgroup = [&](int g) -> int { return g * prm.kblocks / 3; };  // first k-block of group g
+    auto bounce = [&](int j) -> uint32_t {  // k-block j's buffer
+        constexpr int NE = T7_NEPI * T7_EPI_BYTES / 8192;
+        return j < NE ? smem_u32(sEpi) + (uint32_t)j * 8192u
+                      : smem_u32(sF4 + (prm.f4_st - 1) * f4_stage) + (uint32_t)(j - NE) * 8192u;
+    };
+    auto load_filter = [&]() {
+        for (int g = 0; g < 3; ++g) {
+            const int j0 = fgroup(g), j1 = fgroup(g + 1);
+            mbar_arrive_expect_tx(&f_tma[g], (uint32_t)(j1 - j0) * (uint32_t)prm.wrows * 64u);
+            for (int j = j0; j < j1; ++j)
+                tma_load_2d(reinterpret_cast<void*>(smem + (bounce(j) - smem_u32(smem))), &tmap_w, &f_tma[g], j * 64, 0);
+        }
+    };
+
     if (warp == T7_W_PROD) {
-        // ===================== TMA producer: raw halos =====================
+        // ===================== TMA producer: raw halos (and the filter's first round) =====================
         if (lane == 0) {
+            if (my_tiles == 0) load_filter();
             H7Ring rr;
             rr.init(prm.raw_st);
             H7Walk wk;
@@ -220,6 +243,8 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
                 for (int cb = 0; cb < CB; ++cb)
                     tma_load_4d(smem_u32(sRaw + s * raw_stage + cb * prm.raw_cb), &tmap_raw, smem_u32(&raw_full[s]),
                                 cb * 128, -prm.pad, wk.rem * prm.R - prm.pad, wk.img);
+                // the first tile needs its halo (from HBM) and the whole filter: they go out before the second halo
+                if (i == 0) load_filter();
             }
         }
     } else if (warp >= T7_W_CONV && warp < T7_W_PROD) {
@@ -310,7 +335,8 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         for (int i = 0; i < my_tiles; ++i, rr.next(), fr.next()) {
             // the filter's overflow k-blocks bounce through the last fp4 slot (see the epilogue warps):
             // its first converter pass waits until they are in TMEM (long since, in practice)
-            if (i == prm.f4_st - 1) mbar_wait_sleep(f_ready, 0);
+            if (i == prm.f4_st - 1)
+                for (int g = 0; g < 3; ++g) mbar_wait_sleep(&f_ready[g], 0);
             mbar_wait_sleep(&raw_full[rr.idx], rr.phase);
             if (lane == 0) T7_TRACE(1, i);
             mbar_wait_sleep(&a_empty[fr.idx], fr.phase ^ 1);
@@ -328,8 +354,11 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
             const uint32_t d_tmem = tmem_base + (uint32_t)which * T7_BN;
             const uint32_t p4 = (uint32_t)prm.P * 4;  // one halo row in 16-byte units
             const int nkb = prm.kblocks;
-            mbar_wait(f_ready, 0);
-            tc_fence_after();
+            int fg = 0;  // filter groups known to be in TMEM (the first tile of each issuer waits for them as it goes)
+            auto need = [&](int kb) {
+                while (fg < 3 && kb >= fgroup(fg)) mbar_wait(&f_ready[fg++], 0);
+                tc_fence_after();
+            };
             H7Ring fr;
             fr.init(prm.f4_st);
             uint32_t acc_phase = 0;
@@ -345,16 +374,19 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
                 if (lane == 0) {
                     const uint64_t bd0 = h7_desc_sw64(smem_u32(sF4 + fs * f4_stage));
                     // the bias MMA: every accumulator element = 64 * (1.0 * 2^16) * 1.5 = 1.5 * 2^22 (see K7)
+                    if (fg < 3) need(0);
                     umma_mxf4_ts(d_tmem, bias_a, bias_bd, idesc, sf_bias, sf, 0);
                     if (prm.k33) {
 #pragma unroll
                         for (int kb = 0; kb < 9; ++kb) {
+                            if (fg < 3) need(kb);
                             const uint64_t bd = bd0 + (uint32_t)((kb / 3) * p4 + (kb % 3) * 4);
                             umma_mxf4_ts(d_tmem, filt + (uint32_t)kb * 16, bd, idesc, sf, sf, 1);
                             umma_mxf4_ts(d_tmem, filt + (uint32_t)kb * 16 + 8, bd + 2, idesc, sf, sf, 1);
                         }
                     } else {
                         for (int kb = 0; kb < nkb; ++kb) {
+                            if (fg < 3) need(kb);
                             const uint64_t bd = bd0 + kb_boff[kb];
                             umma_mxf4_ts(d_tmem, filt + (uint32_t)kb * 16, bd, idesc, sf, sf, 1);
                             umma_mxf4_ts(d_tmem, filt + (uint32_t)kb * 16 + 8, bd + 2, idesc, sf, sf, 1);
@@ -377,28 +409,13 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
             // The filter into TMEM columns T7_FILT_COL..: lane = output channel n, the row's fp4 bytes
             // (k-block kb, half h at columns 16kb + 8h, the converters' channel order).  Rows are wpitch
             // bytes apart in global memory (a lane loading its own row costs 32 sectors per warp load:
-            // 4,600 L1 cycles per CTA in front of the first tile), so TMA brings each k-block's
-            // 128 rows x 64 B into a bounce buffer — the still idle staging boxes, then the last fp4
-            // slot — in the 64-byte swizzle, whose 16-byte units a quarter-warp reads from eight
+            // 4,600 L1 cycles per CTA in front of the first tile), so TMA brings each k-block into a
+            // bounce buffer in the 64-byte swizzle, whose 16-byte units a quarter-warp reads from eight
             // different banks, and each lane moves its row from there into TMEM.
-            const int cap = T7_NEPI * T7_EPI_BYTES / 8192 + f4_stage / 8192;  // k-blocks per round
-            auto bounce = [&](int j) -> uint32_t {  // buffer j of a round
-                constexpr int NE = T7_NEPI * T7_EPI_BYTES / 8192;
-                return j < NE ? smem_u32(sEpi) + (uint32_t)j * 8192u
-                              : smem_u32(sF4 + (prm.f4_st - 1) * f4_stage) + (uint32_t)(j - NE) * 8192u;
-            };
-            uint32_t round = 0;
-            for (int kb0 = 0; kb0 < prm.kblocks; kb0 += cap, ++round) {
-                const int nk = prm.kblocks - kb0 < cap ? prm.kblocks - kb0 : cap;
-                if (warp == 0 && lane == 0) {
-                    mbar_arrive_expect_tx(f_tma, (uint32_t)nk * (uint32_t)prm.wrows * 64u);
-                    for (int j = 0; j < nk; ++j)
-                        tma_load_2d(reinterpret_cast<void*>(smem + (bounce(j) - smem_u32(smem))), &tmap_w, f_tma,
-                                    (kb0 + j) * 64, 0);
-                }
-                mbar_wait_sleep(f_tma, round & 1);
-                const int r = q * 32 + lane;
-                for (int j = warp >> 2; j < nk; j += 4) {
+            const int r = q * 32 + lane;
+            for (int g = 0; g < 3; ++g) {
+                mbar_wait_sleep(&f_tma[g], 0);
+                for (int j = fgroup(g) + (warp >> 2); j < fgroup(g + 1); j += 4) {
                     uint32_t v[16];
                     const uint32_t src = bounce(j) + (uint32_t)r * 64u;
 #pragma unroll
@@ -406,19 +423,19 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
                         const uint4 x = lds_v4(src + ((uint32_t)(c ^ ((r >> 1) & 3)) << 4));
                         v[4 * c] = x.x, v[4 * c + 1] = x.y, v[4 * c + 2] = x.z, v[4 * c + 3] = x.w;
                     }
-                    tmem_st_32x32b_x16(tmem_base + lane_q + T7_FILT_COL + (uint32_t)(kb0 + j) * 16, v);
+                    tmem_st_32x32b_x16(tmem_base + lane_q + T7_FILT_COL + (uint32_t)j * 16, v);
                 }
-                named_bar_sync(7, 32 * T7_NEPI);  // the bounce buffers are read: the next round (or the first drain) may overwrite them
+                if (g == 0 && warp < 4) {
+                    tmem_st_32x32b_x8_fill(tmem_base + lane_q + T7_SF_COL, 0x7F7F7F7Fu);      // UE8M0 1.0
+                    tmem_st_32x32b_x8_fill(tmem_base + lane_q + T7_SFBIAS_COL, 0x8F8F8F8Fu);  // 2^16: the bias MMA's A scales
+                    tmem_st_32x32b_x8_fill(tmem_base + lane_q + T7_BIAS_COL, 0x22222222u);    // its A operand: e2m1 1.0
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&f_ready[g]);
             }
-            if (warp < 4) {
-                tmem_st_32x32b_x8_fill(tmem_base + lane_q + T7_SF_COL, 0x7F7F7F7Fu);      // UE8M0 1.0
-                tmem_st_32x32b_x8_fill(tmem_base + lane_q + T7_SFBIAS_COL, 0x8F8F8F8Fu);  // 2^16: the bias MMA's A scales
-                tmem_st_32x32b_x8_fill(tmem_base + lane_q + T7_BIAS_COL, 0x22222222u);    // its A operand: e2m1 1.0
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(f_ready);
+            named_bar_sync(7, 32 * T7_NEPI);  // the bounce buffers are read: the first drain may overwrite them
         }
         const uint32_t stg = smem_u32(sEpi) + (uint32_t)warp * T7_EPI_BYTES;
         // stmatrix row addresses: thread t stores position p = 8 * (t / 16) + t % 8 of a 16-position
@@ -502,6 +519,8 @@ TsGeom ts_geom(int h, int w, int c, int cout, int kh, int kw, int stride, int pa
     g.raw_cb = g.rows_h * g.P * 128;
     g.f4_cb = ((g.rows_h * g.P + 8) * 64 + 1023) / 1024 * 1024;  // + the taps' over-read past the halo
     if (g.kblocks > T7_MAX_KB || cb * g.raw_cb > T7_RAW_MAX) return g;
+    // the filter bounces through the staging boxes and the last fp4 slot on its way to TMEM
+    if (g.kblocks > T7_NEPI * T7_EPI_BYTES / 8192 + cb * g.f4_cb / 8192) return g;
     const int budget = T7_SMEM - 1024 - 1024 - T7_BIAS_B - T7_NEPI * T7_EPI_BYTES;  // alignment, barriers, bias operand, staging
     for (int f4 = 3; f4 >= 2; --f4) {
         const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);

@@ -14,5 +14,5 @@ echo LAUNCH=$? >> gpurun_out/r2_pytest.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_fp4_pair -s 1 -c 1 -o gpurun_out/r2_k5_c5 $CMD > gpurun_out/r2_ncu_k5.log 2>&1
 echo FULLK5=$? >> gpurun_out/r2_pytest.log
 timeout 120 python tools/conv_once.py > gpurun_out/r2_conv_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_fp4_halo -s 2 -c 1 -o gpurun_out/r2_k7_c4 python tools/conv_once.py > gpurun_out/r2_ncu_k7.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_fp4_ -s 2 -c 1 -o gpurun_out/r2_k7_c4 python tools/conv_once.py > gpurun_out/r2_ncu_k7.log 2>&1
 echo FULLK7=$? >> gpurun_out/r2_pytest.log
