@@ -830,8 +830,8 @@ def side_configs(lb, torch, flush, pk):
     ops4 = 2.0 * 200704 * 128 * 1152
     res = {}
     conv_paths = (("tensor_fp4", lb.KERNEL_TENSOR, fp4_peak,
-                   "K7: fused halo conv (int8 halo by TMA, e2m1 packed in smem, taps as UMMA row offsets, "
-                   "resident filter, kind::mxf4 pairs), one launch"),
+                   "K7T: fused halo conv (int8 halo by TMA, e2m1 packed in smem, taps as UMMA row offsets, "
+                   "filter resident in tensor memory, kind::mxf4, bias MMA + pack::16b epilogue), one launch"),
                   ("tensor_i8", lb.KERNEL_TENSOR_I8, tensor_peak,
                    "int8 implicit GeMM: im2col TMA over the int8 map -> tcgen05 kind::i8"),
                   ("bitserial", lb.KERNEL_BITSERIAL, popc(1), "K4 fused im2col+encode -> K2 bit-serial"))
