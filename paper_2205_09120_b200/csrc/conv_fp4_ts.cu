@@ -53,10 +53,9 @@
 namespace lb {
 
 constexpr int T7_BN = 128;   // positions per tile (UMMA N)
-constexpr int T7_NCONV = 8;   // converter warps per group
-constexpr int T7_NCG = 2;     // converter groups, on alternate tiles
-constexpr int T7_NEPI = 8;
-constexpr int T7_W_CONV = T7_NEPI, T7_W_PROD = T7_W_CONV + T7_NCG * T7_NCONV, T7_W_MMA = T7_W_PROD + 1,
+constexpr int T7_NCONV = 8;
+constexpr int T7_NEPI = 16;
+constexpr int T7_W_CONV = T7_NEPI, T7_W_PROD = T7_W_CONV + T7_NCONV, T7_W_MMA = T7_W_PROD + 1,
               T7_W_WAIT = T7_W_MMA + 2;
 constexpr int T7_THREADS = 32 * (T7_W_WAIT + 1);
 constexpr int T7_SMEM = 227 * 1024;
@@ -214,9 +213,10 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     // travels in three groups of k-blocks, each with its own barriers, so the first tile's MMAs start
     // on the first third while the rest is still on its way (148 CTAs pull 136 KB each at once).
     auto fgroup = [&](int g) -> int { return g * prm.kblocks / 3; };  // first k-block of group g
-    auto bounce = [&](int j) -> uint32_t {  // k-block j's buffer: the staging boxes, then raw slots 2 and up
+    auto bounce = [&](int j) -> uint32_t {  // k-block j's buffer
         constexpr int NE = T7_NEPI * T7_EPI_BYTES / 8192;
-        return j < NE ? smem_u32(sEpi) + (uint32_t)j * 8192u : smem_u32(sRaw + 2 * raw_stage) + (uint32_t)(j - NE) * 8192u;
+        return j < NE ? smem_u32(sEpi) + (uint32_t)j * 8192u
+                      : smem_u32(sF4 + (prm.f4_st - 1) * f4_stage) + (uint32_t)(j - NE) * 8192u;
     };
     auto load_filter = [&]() {
         for (int g = 0; g < 3; ++g) {
@@ -237,9 +237,6 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
             wk.init((int)blockIdx.x, ncta, prm.tpi);
             for (int i = 0; i < my_tiles; ++i, rr.next(), wk.next()) {
                 const uint32_t s = rr.idx;
-                // raw slots 2 and up carry the filter's bounce buffers until it is in TMEM
-                if (i == 2)
-                    for (int g = 0; g < 3; ++g) mbar_wait_sleep(&f_ready[g], 0);
                 mbar_wait_sleep(&raw_empty[s], rr.phase ^ 1);
                 T7_TRACE(0, i);
                 mbar_arrive_expect_tx(&raw_full[s], (uint32_t)raw_stage);
@@ -252,10 +249,7 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         }
     } else if (warp >= T7_W_CONV && warp < T7_W_PROD) {
         // ===================== converters: raw int8 halo -> fp4 halo (as K7) =====================
-        // two groups of eight warps on alternate tiles: a pass is latency-bound (loads, a dependent
-        // convert chain, stores, the proxy fence, the barrier hand-offs: ~1,800 cycles against 1,216 of
-        // MMA time per tile), so two tiles are converted at once
-        const int cw = (warp - T7_W_CONV) & (T7_NCONV - 1), cg = (warp - T7_W_CONV) / T7_NCONV;
+        const int cw = warp - T7_W_CONV;
         const int P = prm.P, lp = prm.log2p, rows_h = prm.rows_h, raw_st = prm.raw_st, f4_st = prm.f4_st;
         const int raw_cb = prm.raw_cb, f4_cb = prm.f4_cb, R = prm.R;
         const int npos = rows_h * P;             // a multiple of 32
@@ -274,11 +268,8 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         H7Walk wk;
         wk.init((int)blockIdx.x, ncta, prm.tpi);
         for (int i = 0; i < my_tiles; ++i, rr.next(), fr.next(), wk.next()) {
-            if ((i & 1) != cg) continue;  // the other group's tile
             const uint32_t rs = rr.idx, fs = fr.idx;
-            // the waiter saw raw_full and a_empty; one barrier per group and tile parity, so its arrival
-            // for this group's next tile cannot land in this tile's generation
-            named_bar_sync(3 + cg + 2 * ((i >> 1) & 1), 32 * (T7_NCONV + 1));
+            named_bar_sync(3 + rs, 32 * (T7_NCONV + 1));  // the waiter saw raw_full and a_empty
             if (cw == 0 && lane == 0) T7_TRACE(2, i);
             const int ytop = wk.rem * R - prm.pad;  // image row of halo row 0 (binary maps)
             for (int cb = 0; cb < CB; ++cb) {
@@ -342,11 +333,15 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         rr.init(prm.raw_st);
         fr.init(prm.f4_st);
         for (int i = 0; i < my_tiles; ++i, rr.next(), fr.next()) {
+            // the filter's overflow k-blocks bounce through the last fp4 slot (see the epilogue warps):
+            // its first converter pass waits until they are in TMEM (long since, in practice)
+            if (i == prm.f4_st - 1)
+                for (int g = 0; g < 3; ++g) mbar_wait_sleep(&f_ready[g], 0);
             mbar_wait_sleep(&raw_full[rr.idx], rr.phase);
             if (lane == 0) T7_TRACE(1, i);
             mbar_wait_sleep(&a_empty[fr.idx], fr.phase ^ 1);
             __syncwarp();
-            named_bar_arrive(3 + (i & 1) + 2 * ((i >> 1) & 1), 32 * (T7_NCONV + 1));
+            named_bar_arrive(3 + rr.idx, 32 * (T7_NCONV + 1));
         }
     } else if (warp >= T7_W_MMA) {
         // ===================== UMMA issuers: issuer i takes tiles i, i+2, ... into accumulator i =====================
@@ -408,7 +403,7 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         // ===================== epilogue: warps 0-15 =====================
         const int q = warp & 3;               // TMEM lane quarter: output channels 32q .. 32q+31
         const int half = (warp >> 2) & 1;     // positions 64*half .. +63 of the tile
-        // (one group of eight warps drains every tile: accumulator i % 2)
+        const int grp = warp >> 3;            // group: tiles i with i % 2 == grp, accumulator grp
         const uint32_t lane_q = (uint32_t)(q * 32) << 16;
         {
             // The filter into TMEM columns T7_FILT_COL..: lane = output channel n, the row's fp4 bytes
@@ -420,7 +415,7 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
             const int r = q * 32 + lane;
             for (int g = 0; g < 3; ++g) {
                 mbar_wait_sleep(&f_tma[g], 0);
-                for (int j = fgroup(g) + (warp >> 2); j < fgroup(g + 1); j += T7_NEPI / 4) {
+                for (int j = fgroup(g) + (warp >> 2); j < fgroup(g + 1); j += 4) {
                     uint32_t v[16];
                     const uint32_t src = bounce(j) + (uint32_t)r * 64u;
 #pragma unroll
@@ -451,10 +446,10 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         wk.init((int)blockIdx.x, ncta, prm.tpi);
         uint32_t phase = 0;
         for (int i = 0; i < my_tiles; ++i, wk.next()) {
-            const int grp = i & 1;  // the tile's accumulator
+            if ((i & 1) != grp) continue;  // the other group's tile
             if ((warp & 7) == 0) mbar_wait_sleep(&tmem_full[grp], phase);
-            if (grp) phase ^= 1;
-            named_bar_sync(1, 256);
+            phase ^= 1;
+            named_bar_sync(1 + grp, 256);
             tc_fence_after();
             if ((warp & 7) == 0 && lane == 0) T7_TRACE(7, i);
             const int img = wk.img, rt = wk.rem;
@@ -525,11 +520,11 @@ TsGeom ts_geom(int h, int w, int c, int cout, int kh, int kw, int stride, int pa
     g.f4_cb = ((g.rows_h * g.P + 8) * 64 + 1023) / 1024 * 1024;  // + the taps' over-read past the halo
     if (g.kblocks > T7_MAX_KB || cb * g.raw_cb > T7_RAW_MAX) return g;
     // the filter bounces through the staging boxes and the last fp4 slot on its way to TMEM
-    if (g.kblocks > T7_NEPI * T7_EPI_BYTES / 8192 + 2 * cb * g.raw_cb / 8192) return g;
+    if (g.kblocks > T7_NEPI * T7_EPI_BYTES / 8192 + cb * g.f4_cb / 8192) return g;
     const int budget = T7_SMEM - 1024 - 1024 - T7_BIAS_B - T7_NEPI * T7_EPI_BYTES;  // alignment, barriers, bias operand, staging
-    for (int f4 = 3; f4 >= 3; --f4) {  // two tiles in conversion and one under the MMAs; a raw ring of four
+    for (int f4 = 3; f4 >= 2; --f4) {
         const int raw = (budget - f4 * cb * g.f4_cb) / (cb * g.raw_cb);
-        if (raw >= 4) {
+        if (raw >= 2) {
             g.f4_st = f4;
             g.raw_st = raw < T7_MAX_ST ? raw : T7_MAX_ST;
             g.ok = true;
