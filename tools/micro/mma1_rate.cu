@@ -18,13 +18,14 @@ __device__ inline void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32
                  ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(sf) : "memory");
 }
 
-__global__ void __launch_bounds__(128, 1) rate_kernel(int n, int a_in_tmem, int iters, unsigned long long* cyc) {
+__global__ void __launch_bounds__(128, 1) rate_kernel(int n, int a_in_tmem, int iters, unsigned long long* cyc, int nissue) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tslot;
     __shared__ uint64_t bar;
+    __shared__ uint64_t bars4[4];
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < 48 * 1024 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0x2A2A2A2Au;
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) mbar_init(&bars4[i], 1); fence_barrier_init(); }
     if (warp == 0) tmem_alloc<512>(&tslot);
     fence_proxy_async_smem();
     tc_fence_before();
@@ -39,7 +40,18 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int n, int a_in_tmem, int 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (threadIdx.x == 0) {
+    if (nissue > 1) {  // nissue warps issue concurrently, each into its own 128-column accumulator
+        if ((threadIdx.x & 31) == 0 && warp < nissue) {
+            const uint32_t idesc = idesc_mxf4(128, 128);
+            const uint64_t bd = h7_desc_sw64(smem_u32(smem + 16384));
+            const long long t0 = clock64();
+            for (int i = 0; i < iters / nissue; ++i)
+                mma_ts(tb + warp * 128, tb + 400, bd + (uint32_t)((i % 9) * 4), idesc, tb + 504, i != 0);
+            umma_commit(&bars4[warp]);
+            mbar_wait(&bars4[warp], 0);
+            if (warp == 0) cyc[blockIdx.x] = clock64() - t0;
+        }
+    } else if (threadIdx.x == 0) {
         const uint32_t idesc = idesc_mxf4(128, (uint32_t)n);
         const uint64_t ad = h7_desc_sw64(smem_u32(smem)), bd = h7_desc_sw64(smem_u32(smem + 16384));
         const long long t0 = clock64();
@@ -63,12 +75,20 @@ int main() {
     const int iters = 4000;
     for (int n : {128, 256})
         for (int ts : {1, 0}) {
-            rate_kernel<<<148, 128, 64 * 1024>>>(n, ts, iters, cyc);
+            rate_kernel<<<148, 128, 64 * 1024>>>(n, ts, iters, cyc, 1);
             cudaError_t e = cudaDeviceSynchronize();
             unsigned long long h[148];
             cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost);
             printf("cta_group::1 mxf4 M=128 N=%d K=64, A in %s: %.1f cycles per MMA (%s)\n", n, ts ? "TMEM" : "smem",
                    (double)h[0] / iters, cudaGetErrorString(e));
         }
+    for (int k : {2, 3}) {
+        rate_kernel<<<148, 128, 64 * 1024>>>(128, 1, iters, cyc, k);
+        cudaError_t e = cudaDeviceSynchronize();
+        unsigned long long h[148];
+        cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost);
+        printf("%d warps issuing M=128 N=128 TMEM-A MMAs concurrently: %.1f cycles per MMA overall (%s)\n", k,
+               (double)h[0] / iters, cudaGetErrorString(e));
+    }
     return 0;
 }
