@@ -92,6 +92,7 @@ struct TsParams {
 // read by lowbit_debug_ts_trace (the same event numbering as K7's trace)
 __device__ unsigned long long g_ts_trace[16 * 64];
 __device__ unsigned long long g_ts_phase[4];
+__device__ unsigned long long g_ts_cta[160 * 4];  // dbg & 32: per CTA: entry, work start, work end (globaltimer ns), SM id
 LB_DEV unsigned long long t7_gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -139,7 +140,13 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
                        const __grid_constant__ CUtensorMap tmap_w, const TsParams prm) {
     constexpr bool PADFILL = (FLAGS & 1) != 0, CHECKZ = (FLAGS & 2) != 0;
     if (T7_DBG(32768)) return;
-    if (T7_DBG(32) && threadIdx.x == 0) atomicMin(&g_ts_phase[0], t7_gtime());
+    if (T7_DBG(32) && threadIdx.x == 0) {
+        atomicMin(&g_ts_phase[0], t7_gtime());
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_ts_cta[blockIdx.x * 4] = t7_gtime();
+        g_ts_cta[blockIdx.x * 4 + 3] = smid;
+    }
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int CB = prm.cblocks;
@@ -206,7 +213,10 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     // the next kernel in the stream may begin launching; global memory is touched only after the wait
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (T7_DBG(32) && threadIdx.x == 0) atomicMax(&g_ts_phase[1], t7_gtime());
+    if (T7_DBG(32) && threadIdx.x == 0) {
+        atomicMax(&g_ts_phase[1], t7_gtime());
+        g_ts_cta[blockIdx.x * 4 + 1] = t7_gtime();
+    }
 
     // The filter's way into TMEM: TMA brings each k-block's 128 rows x 64 B into a bounce buffer — the
     // still idle staging boxes, then the last fp4 slot — and the epilogue warps move it on (below).  It
@@ -492,7 +502,10 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (T7_DBG(32) && threadIdx.x == 0) atomicMax(&g_ts_phase[2], t7_gtime());
+    if (T7_DBG(32) && threadIdx.x == 0) {
+        atomicMax(&g_ts_phase[2], t7_gtime());
+        g_ts_cta[blockIdx.x * 4 + 2] = t7_gtime();
+    }
     if (warp == T7_W_MMA) {
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
@@ -618,6 +631,9 @@ lowbit_status launch_conv_ts(const int8_t* fm, int batch, int h, int w, int cch,
 
 extern "C" int lowbit_debug_ts_trace(unsigned long long* out1024) {
     return cudaMemcpyFromSymbol(out1024, lb::g_ts_trace, sizeof(unsigned long long) * 1024) != cudaSuccess;
+}
+extern "C" int lowbit_debug_ts_ctas(unsigned long long* out640) {
+    return cudaMemcpyFromSymbol(out640, lb::g_ts_cta, sizeof(unsigned long long) * 640) != cudaSuccess;
 }
 extern "C" int lowbit_debug_ts_phases(unsigned long long* out4, int reset) {
     if (cudaMemcpyFromSymbol(out4, lb::g_ts_phase, sizeof(unsigned long long) * 4) != cudaSuccess) return 1;
