@@ -92,6 +92,7 @@ struct TsParams {
 // read by lowbit_debug_ts_trace (the same event numbering as K7's trace)
 __device__ unsigned long long g_ts_trace[16 * 64];
 __device__ unsigned long long g_ts_phase[4];
+__device__ unsigned long long g_ts_setup[160 * 4];  // dbg & 32: per CTA: barriers initialised, TMEM allocated, CTA barrier passed
 __device__ unsigned long long g_ts_cta[160 * 4];  // dbg & 32: per CTA: entry, work start, work end (globaltimer ns), SM id
 LB_DEV unsigned long long t7_gtime() {
     unsigned long long t;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
             mbar_init(&f_tma[g], 1);
         }
         fence_barrier_init();
+        if (T7_DBG(32)) g_ts_setup[blockIdx.x * 4] = t7_gtime();
     }
     if (threadIdx.x < T7_BIAS_B / 16)  // every B element of the bias MMA is e2m1 1.5
         sts_v4(smem_u32(sBiasB) + threadIdx.x * 16, 0x33333333u, 0x33333333u, 0x33333333u, 0x33333333u);
@@ -200,6 +202,7 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     }
     if (warp == T7_W_MMA) {
         tmem_alloc<512>(tmem_slot);
+        if (T7_DBG(32) && lane == 0) g_ts_setup[blockIdx.x * 4 + 1] = t7_gtime();
         for (int kb = lane; kb < prm.kblocks; kb += 32) {  // tap (ky,kx), channel block cb
             const int tap = kb / CB, cb = kb - tap * CB;
             const int ky = tap / prm.kw, kx = tap - ky * prm.kw;
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (T7_DBG(32) && threadIdx.x == 0) g_ts_setup[blockIdx.x * 4 + 2] = t7_gtime();
     // the next kernel in the stream may begin launching; global memory is touched only after the wait
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -634,6 +638,9 @@ extern "C" int lowbit_debug_ts_trace(unsigned long long* out1024) {
 }
 extern "C" int lowbit_debug_ts_ctas(unsigned long long* out640) {
     return cudaMemcpyFromSymbol(out640, lb::g_ts_cta, sizeof(unsigned long long) * 640) != cudaSuccess;
+}
+extern "C" int lowbit_debug_ts_setup(unsigned long long* out640) {
+    return cudaMemcpyFromSymbol(out640, lb::g_ts_setup, sizeof(unsigned long long) * 640) != cudaSuccess;
 }
 extern "C" int lowbit_debug_ts_phases(unsigned long long* out4, int reset) {
     if (cudaMemcpyFromSymbol(out4, lb::g_ts_phase, sizeof(unsigned long long) * 4) != cudaSuccess) return 1;

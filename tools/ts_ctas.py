@@ -24,3 +24,9 @@ d12 = sorted(r[2] - r[1] for i, r in enumerate(rows) if i >= 1792 - 12 * 148)
 print("13-tile CTAs work duration ns:", d13[0], q(d13, .5), d13[-1], "| 12-tile CTAs:", d12[0], q(d12, .5), d12[-1])
 late = sorted(rows, key=lambda r: -r[2])[:8]
 print("latest CTAs (block, sm, entry, end):", [(rows.index(r), r[3], r[0] - t0, r[2] - t0) for r in late])
+sb = (C.c_ulonglong * 640)()
+if hasattr(lb._lib.lib, "lowbit_debug_ts_setup") and lb._lib.lib.lowbit_debug_ts_setup(sb) == 0:
+    a = sorted(sb[4 * i] - rows[i][0] for i in range(148)); b = sorted(sb[4 * i + 1] - rows[i][0] for i in range(148))
+    c = sorted(sb[4 * i + 2] - rows[i][0] for i in range(148))
+    print("setup, ns after the CTA's entry (median / max): barriers initialised %d / %d, TMEM allocated %d / %d, CTA barrier passed %d / %d"
+          % (q(a, .5), a[-1], q(b, .5), b[-1], q(c, .5), c[-1]))
