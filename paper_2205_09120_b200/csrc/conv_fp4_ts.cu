@@ -174,7 +174,29 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
     const int ncta = gridDim.x;
     const int my_tiles = prm.ctiles > (int)blockIdx.x ? (prm.ctiles - (int)blockIdx.x + ncta - 1) / ncta : 0;
 
-    if (threadIdx.x == 0) {
+    // The filter's way into TMEM: TMA brings each k-block's 128 rows x 64 B into a bounce buffer — the
+    // still idle staging boxes, then the last fp4 slot — and the epilogue warps move it on (below).  It
+    // travels in three groups of k-blocks, each with its own barriers, so the first tile's MMAs start
+    // on the first third while the rest is still on its way (148 CTAs pull 136 KB each at once).
+    auto fgroup = [&](int g) -> int { return g * prm.kblocks / 3; };  // first k-block of group g
+    auto bounce = [&](int j) -> uint32_t {  // k-block j's buffer
+        constexpr int NE = T7_NEPI * T7_EPI_BYTES / 8192;
+        return j < NE ? smem_u32(sEpi) + (uint32_t)j * 8192u
+                      : smem_u32(sF4 + (prm.f4_st - 1) * f4_stage) + (uint32_t)(j - NE) * 8192u;
+    };
+    auto load_filter = [&]() {
+        for (int g = 0; g < 3; ++g) {
+            const int j0 = fgroup(g), j1 = fgroup(g + 1);
+            mbar_arrive_expect_tx(&f_tma[g], (uint32_t)(j1 - j0) * (uint32_t)prm.wrows * 64u);
+            for (int j = j0; j < j1; ++j)
+                tma_load_2d(reinterpret_cast<void*>(smem + (bounce(j) - smem_u32(smem))), &tmap_w, &f_tma[g], j * 64, 0);
+        }
+    };
+
+    // The producer thread initialises the barriers and at once sends the first tile's halo and the
+    // filter on their way (its own griddepcontrol.wait orders them after the previous grid): they
+    // gate the first tile, and the rest of the setup (TMEM, the CTA barrier) takes another ~0.5 us.
+    if (warp == T7_W_PROD && lane == 0) {
         for (int s = 0; s < T7_MAX_ST; ++s) {
             mbar_init(&raw_full[s], 1);
             mbar_init(&raw_empty[s], T7_NCONV);
@@ -191,15 +213,23 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         }
         fence_barrier_init();
         if (T7_DBG(32)) g_ts_setup[blockIdx.x * 4] = t7_gtime();
+        tma_prefetch_desc(&tmap_raw);
+        tma_prefetch_desc(&tmap_w);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (my_tiles > 0) {
+            H7Walk wk;
+            wk.init((int)blockIdx.x, ncta, prm.tpi);
+            mbar_arrive_expect_tx(&raw_full[0], (uint32_t)raw_stage);
+            for (int cb = 0; cb < CB; ++cb)
+                tma_load_4d(smem_u32(sRaw + cb * prm.raw_cb), &tmap_raw, smem_u32(&raw_full[0]), cb * 128, -prm.pad,
+                            wk.rem * prm.R - prm.pad, wk.img);
+        }
+        load_filter();
     }
     if (threadIdx.x < T7_BIAS_B / 16)  // every B element of the bias MMA is e2m1 1.5
         sts_v4(smem_u32(sBiasB) + threadIdx.x * 16, 0x33333333u, 0x33333333u, 0x33333333u, 0x33333333u);
     fence_proxy_async_smem();
-    if (warp == T7_W_PROD && lane == 0) {
-        tma_prefetch_desc(&tmap_raw);
-        tma_prefetch_desc(&tmap_out);
-        tma_prefetch_desc(&tmap_w);
-    }
+    if (warp == T7_W_PROD && lane == 1) tma_prefetch_desc(&tmap_out);
     if (warp == T7_W_MMA) {
         tmem_alloc<512>(tmem_slot);
         if (T7_DBG(32) && lane == 0) g_ts_setup[blockIdx.x * 4 + 1] = t7_gtime();
@@ -222,43 +252,25 @@ __global__ void __launch_bounds__(T7_THREADS, 1)
         g_ts_cta[blockIdx.x * 4 + 1] = t7_gtime();
     }
 
-    // The filter's way into TMEM: TMA brings each k-block's 128 rows x 64 B into a bounce buffer — the
-    // still idle staging boxes, then the last fp4 slot — and the epilogue warps move it on (below).  It
-    // travels in three groups of k-blocks, each with its own barriers, so the first tile's MMAs start
-    // on the first third while the rest is still on its way (148 CTAs pull 136 KB each at once).
-    auto fgroup = [&](int g) -> int { return g * prm.kblocks / 3; };  // first k-block of group g
-    auto bounce = [&](int j) -> uint32_t {  // k-block j's buffer
-        constexpr int NE = T7_NEPI * T7_EPI_BYTES / 8192;
-        return j < NE ? smem_u32(sEpi) + (uint32_t)j * 8192u
-                      : smem_u32(sF4 + (prm.f4_st - 1) * f4_stage) + (uint32_t)(j - NE) * 8192u;
-    };
-    auto load_filter = [&]() {
-        for (int g = 0; g < 3; ++g) {
-            const int j0 = fgroup(g), j1 = fgroup(g + 1);
-            mbar_arrive_expect_tx(&f_tma[g], (uint32_t)(j1 - j0) * (uint32_t)prm.wrows * 64u);
-            for (int j = j0; j < j1; ++j)
-                tma_load_2d(reinterpret_cast<void*>(smem + (bounce(j) - smem_u32(smem))), &tmap_w, &f_tma[g], j * 64, 0);
-        }
-    };
-
     if (warp == T7_W_PROD) {
         // ===================== TMA producer: raw halos (and the filter's first round) =====================
         if (lane == 0) {
-            if (my_tiles == 0) load_filter();
             H7Ring rr;
             rr.init(prm.raw_st);
             H7Walk wk;
             wk.init((int)blockIdx.x, ncta, prm.tpi);
             for (int i = 0; i < my_tiles; ++i, rr.next(), wk.next()) {
                 const uint32_t s = rr.idx;
+                if (i == 0) {  // sent before the setup
+                    T7_TRACE(0, i);
+                    continue;
+                }
                 mbar_wait_sleep(&raw_empty[s], rr.phase ^ 1);
                 T7_TRACE(0, i);
                 mbar_arrive_expect_tx(&raw_full[s], (uint32_t)raw_stage);
                 for (int cb = 0; cb < CB; ++cb)
                     tma_load_4d(smem_u32(sRaw + s * raw_stage + cb * prm.raw_cb), &tmap_raw, smem_u32(&raw_full[s]),
                                 cb * 128, -prm.pad, wk.rem * prm.R - prm.pad, wk.img);
-                // the first tile needs its halo (from HBM) and the whole filter: they go out before the second halo
-                if (i == 0) load_filter();
             }
         }
     } else if (warp >= T7_W_CONV && warp < T7_W_PROD) {
