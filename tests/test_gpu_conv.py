@@ -227,6 +227,28 @@ def test_conv_halo_column_blocks(lb, port, mode):
             lb.conv2d_lowbit(BNN, torch.from_numpy(fm).cuda(), True, weights_for(lb, wt, BNN), 3, 3, 1, 1)
 
 
+@pytest.mark.parametrize("mode", [TNN, TBN])
+def test_conv_halo_filter_sizes(lb, port, mode):
+    """The halo convs across filter depths: K7T keeps the filter in tensor memory (cout <= 128, up to 14
+    k-blocks of 128 channels that also fit its bounce buffers) and loads it in three barrier groups; K7
+    takes the rest.  1x1 and 2x2 filters over 1-4 channel blocks (1, 2, 3, 4, 8, 12, 16 k-blocks), cout
+    from 8 to 136, each against the oracle's direct convolution."""
+    da, db = mode_dists(mode)
+    cases = [(2, 8, 20, 128, 128, 1), (2, 8, 20, 256, 40, 1), (1, 9, 30, 384, 8, 1), (3, 6, 12, 128, 96, 2),
+             (2, 7, 16, 256, 128, 2), (1, 6, 10, 384, 64, 2), (1, 5, 9, 512, 136, 2), (2, 5, 40, 512, 24, 1)]
+    for i, (b, h, w, ch, cout, ksz) in enumerate(cases):
+        # (three or four channel blocks can outgrow the halo kernels' shared memory: K6 takes those)
+        path = lb.conv_select(mode, False, b, h, w, ch, cout, ksz, ksz, 1, 0)
+        assert path == lb.CONV_PATH_HALO_FP4 or (ch >= 384 and path == lb.CONV_PATH_IMPLICIT_FP4), path
+        fm = port.generate(da, 250 + i, 0, b * h * w, ch).reshape(b, h, w, ch)
+        wt = port.generate(db, 250 + i, 1, ksz * ksz * ch, cout)
+        got = lb.conv2d_lowbit(mode, torch.from_numpy(fm).cuda(), False, weights_for(lb, wt, mode), ksz, ksz, 1,
+                               0).cpu().numpy()
+        for img in range(b):
+            want = port.direct_conv(fm[img], False, wt, ksz, ksz, 1, 0)
+            assert (got[img].astype(np.int32) == want).all(), (mode, b, h, w, ch, cout, ksz, img)
+
+
 @pytest.mark.parametrize("ch", [32, 40])
 def test_conv_binary_zero_only_where_sampled(lb, port, ch):
     """ZeroInBinaryInput follows im2col's view (conv.cpp:9-31, core.cpp:23): a 0 in a
