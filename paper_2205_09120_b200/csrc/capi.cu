@@ -133,10 +133,16 @@ static lowbit_status validate_gemm(int mode, bool a_ternary, int b_ternary, int 
 extern "C" int lowbit_select_kernel(int mode, int m, int n, int k) {
     (void)mode;
     const double ops = 2.0 * (double)m * (double)n * (double)k;
-    // launch-bound shapes (< ~1 GOP): the int8 kernel; up to 4 row tiles the single-CTA
-    // variant (its smaller launch: config 1 4.4 vs 5.2 us per call; the config-2 sweep is
-    // a tie, tools/c1_latency.py); above that the fp4 kernel
-    if (ops < 1e9) return m <= 512 ? LOWBIT_KERNEL_TENSOR_1CTA : LOWBIT_KERNEL_TENSOR_I8;
+    // Launch-bound shapes (< ~1 GOP), measured per call in a graph of back-to-back calls with every
+    // kernel launched as a programmatic dependent (tools/c1_latency.py, PER_SHAPE=1; the 64 shapes of
+    // config 2 take 250.7 us by this rule, 247.5 by the per-shape best, 286.1 on the single-CTA kernel
+    // alone): outputs at least 96 columns wide take the int8 kernel, single-CTA up to 4 row tiles
+    // (config 1: 3.5 us against 3.9 on the fp4 kernel); narrower ones the fp4 pair kernel, or the
+    // int8 one when the depth is a single k-block.  Above that the fp4 kernel.
+    if (ops < 1e9) {
+        if (n >= 96) return m <= 512 ? LOWBIT_KERNEL_TENSOR_1CTA : LOWBIT_KERNEL_TENSOR_I8;
+        return k <= 128 ? LOWBIT_KERNEL_TENSOR_I8 : LOWBIT_KERNEL_TENSOR;
+    }
     return LOWBIT_KERNEL_TENSOR;
 }
 

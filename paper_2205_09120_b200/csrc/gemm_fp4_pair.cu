@@ -267,6 +267,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(F4_THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // programmatic dependent launch: the next kernel in the stream may begin launching (and run its
+    // setup) now; this grid touches global memory only after its own wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == F4_W_RAW) {
         // ===================== raw A-plane producer (both CTAs) =====================
@@ -799,7 +803,17 @@ static lowbit_status launch_fp4_variant(const CUtensorMap& mb, const CUtensorMap
     if (verbose)
         std::fprintf(stderr, "fp4 kernel: AR %d CL %d grid %d (max clusters %d) bn %d n_tiles %d m_tiles %d\n",
                      (int)AR, CL, grid, max_clusters, prm.bn, prm.n_tiles, prm.m_tiles);
-    kern<<<grid, F4_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(F4_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mb, ma0, ma1, mc, prm));
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

@@ -86,6 +86,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: the next kernel in the stream may begin launching now (its CTAs
+    // run their setup while this grid works, then block in their own griddepcontrol.wait until this
+    // grid has completed); this grid touches global memory only after its wait.  Launch-bound shapes
+    // (config 1) are mostly launch latency and setup.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -217,7 +223,17 @@ static lowbit_status launch_tc_variant(const CUtensorMap& mb, const CUtensorMap&
                                        const TcParams& prm, int grid, cudaStream_t stream) {
     static SmemOptIn attr;
     LB_CUDA_TRY(attr.ensure(gemm_tc_kernel<A_TER, LAYOUT>, TC_SMEM_BYTES));
-    gemm_tc_kernel<A_TER, LAYOUT><<<grid, TC_THREADS, TC_SMEM_BYTES, stream>>>(mb, ma0, ma1, prm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = TC_SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LB_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<A_TER, LAYOUT>, mb, ma0, ma1, prm));
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

@@ -147,6 +147,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // programmatic dependent launch: the next kernel in the stream may begin launching (and run its
+    // setup) now; this grid touches global memory only after its own wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == PR_W_RAW) {
         // ===================== raw A-bit producer (both CTAs) =====================
@@ -464,7 +468,17 @@ static lowbit_status launch_pair_variant(const CUtensorMap& mb, const CUtensorMa
     static SmemOptIn attr;
     LB_CUDA_TRY(attr.ensure(gemm_tc_pair_kernel<A_TER, LAYOUT>, PR_SMEM_LIMIT));
     const int smem = pr_smem_bytes(prm.a_stages, prm.b_stages, prm.raw_stages);
-    gemm_tc_pair_kernel<A_TER, LAYOUT><<<2 * pairs, PR_THREADS, smem, stream>>>(mb, ma0, ma1, mc, prm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(PR_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LB_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_pair_kernel<A_TER, LAYOUT>, mb, ma0, ma1, mc, prm));
     LB_CUDA_TRY(cudaGetLastError());
     return LOWBIT_OK;
 }

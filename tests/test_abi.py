@@ -81,9 +81,11 @@ def test_select_kernel_table():
     assert L.lib.lowbit_select_kernel(L.TNN, 1048576, 1024, 2048) == L.KERNEL_TENSOR
     assert L.lib.lowbit_select_kernel(L.BNN, 8192, 8192, 4096) == L.KERNEL_TENSOR
     # launch-bound shapes take the int8 tensor kernel (c1, the c2 sweep)
-    assert L.lib.lowbit_select_kernel(L.TBN, 72, 24, 128) == L.KERNEL_TENSOR_1CTA
+    assert L.lib.lowbit_select_kernel(L.TBN, 72, 24, 128) == L.KERNEL_TENSOR_I8   # one k-block, narrow output
+    assert L.lib.lowbit_select_kernel(L.TBN, 72, 24, 512) == L.KERNEL_TENSOR      # narrow output: the fp4 kernel
     assert L.lib.lowbit_select_kernel(L.TNN, 360, 96, 256) == L.KERNEL_TENSOR_1CTA
-    assert L.lib.lowbit_select_kernel(L.TNN, 4096, 64, 512) == L.KERNEL_TENSOR_I8
+    assert L.lib.lowbit_select_kernel(L.TNN, 4096, 128, 256) == L.KERNEL_TENSOR_I8
+    assert L.lib.lowbit_select_kernel(L.TNN, 4096, 64, 512) == L.KERNEL_TENSOR
 
 
 def test_conv_select_paths():

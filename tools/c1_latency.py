@@ -44,11 +44,15 @@ for M, N, K in itertools.product((72, 120, 240, 360), (24, 48, 72, 96), (128, 25
     c = torch.empty((M, N), dtype=torch.int16, device="cuda")
     ref = lb.gemm_lowbit(lb.TBN, ap, w, (M, N, K), kernel=lb.KERNEL_BITSERIAL)
     best, bestk = 1e9, None
+    row = {}
     for name, kern in [("tensor_i8", lb.KERNEL_TENSOR_I8), ("1cta", lb.KERNEL_TENSOR_1CTA), ("tensor", lb.KERNEL_TENSOR)]:
         us = graph_us(lambda: lb.gemm_lowbit(lb.TBN, ap, w, (M, N, K), kernel=kern, out=c), reps=20)
         assert torch.equal(c, ref), (M, N, K, name)
         tot[name] += us
+        row[name] = us
         if us < best:
             best, bestk = us, name
     wins[bestk] += 1
+    if os.environ.get("PER_SHAPE"):
+        print(M, N, K, " ".join(f"{k}={v:.2f}" for k, v in row.items()), "best", bestk)
 print("c2 sweep, sum of per-shape latencies (us):", {k: round(v, 1) for k, v in tot.items()}, "wins:", wins)
