@@ -384,7 +384,9 @@ extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int 
                          (a_binary || (reinterpret_cast<uintptr_t>(plane1) & 15) == 0) && (pitch & 15) == 0;
     if (c % 32 == 0 && kh < 256 && kw < 256 && ring_smem <= 96 * 1024 && aligned && (long long)w * (c / 32) < (1 << 24)) {
         static SmemOptIn ring_attr;
-        if (ring_smem > 48 * 1024) LB_CUDA_TRY(ring_attr.ensure(conv_encode_ring_kernel, 96 * 1024));
+        // (the 48 KB a kernel gets without the opt-in counts its static shared memory too — the
+        // kernel's 1 KB tap-row table: tools/fuzz_conv.py found a 48,496-byte ring failing to launch)
+        if (ring_smem > 44 * 1024) LB_CUDA_TRY(ring_attr.ensure(conv_encode_ring_kernel, 96 * 1024));
         const long long orows = (long long)batch * g.oh;
         // K4_BLOCKS_PER_SM co-resident blocks per SM, each a contiguous run of output rows (it
         // re-encodes kh - stride input rows at its start)
@@ -394,7 +396,7 @@ extern "C" lowbit_status lowbit_conv_encode(int a_binary, const int8_t* fm, int 
             a_binary, fm, g, pad_value, plane0, plane1, pitch, zero_flag);
     } else if (c % 32 == 0 && kh < 256 && kw < 256 && smem <= 160 * 1024 && (reinterpret_cast<uintptr_t>(fm) & 15) == 0) {
         static SmemOptIn attr;
-        if (smem > 48 * 1024) LB_CUDA_TRY(attr.ensure(conv_encode_rows_kernel, (int)smem));
+        if (smem > 44 * 1024) LB_CUDA_TRY(attr.ensure(conv_encode_rows_kernel, (int)smem));
         const long long orows = (long long)batch * g.oh;
         const int blocks = (int)(orows < 148LL * 8 ? orows : 148LL * 8);
         conv_encode_rows_kernel<<<blocks, 256, (size_t)smem, (cudaStream_t)stream>>>(a_binary, fm, g, pad_value,

@@ -349,3 +349,17 @@ def test_conv_halo_large_sums(lb, port, mode):
             want = port.direct_conv(fm[img], False, wt, ksz, ksz, 1, pad)
             assert (got[img].astype(np.int32) == want).all(), (mode, c, ksz)
         assert np.abs(got).max() > 1500
+
+
+def test_conv_fuzz_against_reference_semantics(lb):
+    """tools/fuzz_conv.py for 20 s: seeded random stride-1 convs (every mode, binary maps with every pad
+    value, int8 values mapped by sign, widths past 128, 1-3 channel blocks, cout up to 312) through
+    conv2d_lowbit against the oracle's im2col -> encode -> GeMM (conv.cpp:33-59)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SECONDS="20", SEED="7")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_conv.py")], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "fuzz OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
